@@ -1,0 +1,143 @@
+/* include/coat.h -- the drop-in C-ABI of the B200-native COAT hot path.
+ *
+ * Every entry point replaces one operator of the reference's proj/core API
+ * (coatsim, /root/reference/proj/core/include/coatsim/*.hpp); the comment on
+ * each cites the reference declaration (file:line) it stands in for.  The
+ * reference is a C++ library with no FFI of its own, so this header is the
+ * boundary a binding (ctypes, the C++ shim in include/coat/coatsim_compat.hpp,
+ * a JNI/cgo stub) links against; INTEGRATION.md shows those bindings.
+ *
+ * Conventions
+ *  - Plain C: extern "C", no exceptions cross this boundary, no CUDA/torch
+ *    types in the signatures.  `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).
+ *  - All tensor pointers are caller-owned DEVICE buffers (cudaMalloc'ed or
+ *    torch storage) with explicit element counts; calls are asynchronous and
+ *    stream-ordered.
+ *  - Errors the reference raises from shapes/geometry are returned
+ *    synchronously.  Data-dependent errors (non-finite values) are OR-ed as
+ *    bits into a caller-provided device word `d_flags` (may be NULL);
+ *    coat_flags_to_status() maps the word to the status the reference's
+ *    exception would correspond to (errors.hpp:8-22).
+ *  - Scales are stored as BF16 bit patterns (uint16_t): the reference's scales
+ *    are always BF16-valued (quantize.cpp:10-17), so this is lossless.
+ *  - dtype codes: 0 = fp32, 1 = bf16.
+ */
+#ifndef COAT_H
+#define COAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes, 1:1 with the reference exception taxonomy (errors.hpp:8-22). */
+typedef enum coat_status {
+    COAT_OK = 0,
+    COAT_ERR_SHAPE = 1,             /* ShapeMismatch                     */
+    COAT_ERR_GEOMETRY = 2,          /* GeometryMismatch                  */
+    COAT_ERR_NONFINITE_INPUT = 3,   /* NonFiniteInput                    */
+    COAT_ERR_NONFINITE_GRAD = 4,    /* NonFiniteGradient                 */
+    COAT_ERR_INVALID = 5,           /* InvalidSpec                       */
+    COAT_ERR_CUDA = 6,              /* (new) CUDA runtime error          */
+    COAT_ERR_NCCL = 7,              /* (new) NCCL error                  */
+    COAT_ERR_OUT_OF_RANGE = 8,      /* OutOfRange                        */
+    COAT_ERR_ALL_ZERO_GROUP = 9,    /* AllZeroGroup                      */
+    COAT_ERR_IO = 10,               /* IoError                           */
+    COAT_ERR_BAD_MAGIC = 11         /* BadMagic                          */
+} coat_status;
+
+/* Device flag bits OR-ed into d_flags. */
+#define COAT_FLAG_NONFINITE_INPUT 1u
+#define COAT_FLAG_NONFINITE_GRAD 2u
+#define COAT_FLAG_PACK_M 4u        /* pack_moment(m) would throw (optimizer.cpp:111) */
+#define COAT_FLAG_PACK_V 8u        /* pack_moment(v) would throw (optimizer.cpp:112) */
+#define COAT_FLAG_CONTRACT 16u     /* non-finite state on unpack (expand.cpp:104)    */
+
+/* One moment of an E4M3 + DRE optimizer state, 1x128 groups
+ * (ExpandedQuantState, expand.hpp:60-63 + QuantizedTensor, quantize.hpp:37-46). */
+typedef struct coat_moment_state {
+    uint8_t* codes;     /* [npad]   npad = ceil(n/128)*128 */
+    uint16_t* scales;   /* [npad/128] BF16 bit patterns    */
+    float* k;           /* [npad/128] expansion exponent   */
+    float* c;           /* [npad/128] stabilizer           */
+} coat_moment_state;
+
+/* AdamWConfig (optimizer.hpp:13-20) minus the step counter (passed as t). */
+typedef struct coat_adamw_config {
+    float beta1, beta2, lr, weight_decay, eps;
+} coat_adamw_config;
+
+const char* coat_version(void);
+const char* coat_status_string(coat_status s);
+const char* coat_last_error(void);
+coat_status coat_flags_to_status(uint32_t flags);
+int coat_device_sm_count(void);
+
+/* ---------------------------------------------------------------- codec -- */
+/* encode_byte(x, e4m3) elementwise (fp8.hpp:47, fp8.cpp:150-156). */
+coat_status coat_encode_e4m3(const float* x, uint8_t* codes, int64_t n, uint32_t* d_flags,
+                             void* stream);
+/* decode_byte(code, e4m3) elementwise (fp8.hpp:48, fp8.cpp:145-148). */
+coat_status coat_decode_e4m3(const uint8_t* codes, float* x, int64_t n, void* stream);
+
+/* ------------------------------------------------------------ quantizer -- */
+/* quantize(x, per_group(G), e4m3) on a [rows x cols] tensor (quantize.hpp:70-71);
+ * GeometryMismatch unless cols % G == 0.  scales: [rows*cols/G]. */
+coat_status coat_quantize_per_group(const void* x, int dtype, int64_t rows, int64_t cols,
+                                    int64_t group_size, uint8_t* codes, uint16_t* scales,
+                                    uint32_t* d_flags, void* stream);
+/* dequantize(QuantizedTensor) for per-group geometry (quantize.hpp:72). */
+coat_status coat_dequantize_per_group(const uint8_t* codes, const uint16_t* scales, int64_t rows,
+                                      int64_t cols, int64_t group_size, void* out, int out_dtype,
+                                      void* stream);
+/* group_scale_max(x, G) (quantize.hpp:77): stage 1 per-1xG absmax into
+ * `intermediate` [rows*cols/G] (may be NULL), stage 2 global max written as
+ * fp32 bits to *d_amax_bits (device). */
+coat_status coat_group_scale_max(const void* x, int dtype, int64_t rows, int64_t cols,
+                                 int64_t group_size, float* intermediate, uint32_t* d_amax_bits,
+                                 void* stream);
+/* quantize(x, per_tensor, e4m3) given the absmax from coat_group_scale_max
+ * (quantize.hpp:70-71); writes the BF16 scale to *d_scale (device). */
+coat_status coat_quantize_per_tensor(const void* x, int dtype, int64_t n,
+                                     const uint32_t* d_amax_bits, uint8_t* codes,
+                                     uint16_t* d_scale, uint32_t* d_flags, void* stream);
+/* dequantize(QuantizedTensor) for per-tensor geometry (quantize.hpp:72). */
+coat_status coat_dequantize_per_tensor(const uint8_t* codes, const uint16_t* d_scale, int64_t n,
+                                       void* out, int out_dtype, void* stream);
+
+/* ------------------------------------------------------ range expansion -- */
+/* expand_quantize(x, G=128, e4m3) on a flat tensor (expand.hpp:67-68);
+ * GeometryMismatch unless n % G == 0; InvalidSpec for G != 128. */
+coat_status coat_expand_quantize(const float* x, int64_t n, int64_t group_size,
+                                 coat_moment_state out, uint32_t* d_flags, void* stream);
+/* dequantize_contract(state) (expand.hpp:71). */
+coat_status coat_dequantize_contract(coat_moment_state in, int64_t n, int64_t group_size,
+                                     float* x, uint32_t* d_flags, void* stream);
+
+/* ------------------------------------------------------------ optimizer -- */
+/* make_slot(shape, {E4M3, expand, G} x2) (optimizer.hpp:54) for n params. */
+coat_status coat_make_slot(int64_t n, int64_t group_size, coat_moment_state m,
+                           coat_moment_state v, void* stream);
+/* step(params, grads, slot, cfg) (optimizer.hpp:58) as ONE fused kernel:
+ * reads w_in, g and the (m_in, v_in) state, writes w_out and (m_out, v_out).
+ * t is the 1-based step being applied (slot.step + 1).  w_out may alias w_in
+ * and *_out may alias *_in (in-place), but then a non-finite gradient can no
+ * longer leave the parameters untouched as the reference guarantees
+ * (optimizer.cpp:104); the ping-pong form keeps that guarantee. */
+coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n,
+                                int64_t group_size, coat_moment_state m_in,
+                                coat_moment_state v_in, coat_moment_state m_out,
+                                coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t,
+                                uint32_t* d_flags, void* stream);
+
+/* Test/diagnostic hook: count elements that took the literal (double pow)
+ * fallback in DRE kernels into *d_counter (device u64); NULL disables. */
+coat_status coat_set_fallback_counter(unsigned long long* d_counter);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COAT_H */

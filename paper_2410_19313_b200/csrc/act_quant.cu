@@ -1,0 +1,394 @@
+// act_quant.cu -- K2/K3: Mixed-Granularity Activation Quantization (MGAQ)
+// kernels and the flat E4M3 codec, for sm_100a.
+//
+// Reference (paths relative to /root/reference/proj/core/src):
+//   quantize / dequantize      quantize.cpp:89-124  (per-tensor and per-group 1xG)
+//   group_scale_max            quantize.cpp:126-145 (two-stage Group Scaling amax)
+//   encode_byte / decode_byte  fp8.cpp:145-156
+// Call sites: FlowCtx::save_nonlinear (per-group, flow.cpp:450-456) and
+// save_linear (per-tensor, flow.cpp:469-474).
+//
+// All kernels are HBM-bound streams.  A thread owns a 16-element chunk
+// (32 B of bf16 or 64 B of fp32 in, one 16 B vector of codes out); a 1xG group
+// spans G/16 consecutive lanes and its absmax is a log2(G/16)-step xor-shuffle
+// max.  Codes are certified against the exact IEEE quotient x/s
+// (certified_code in coat_device.cuh) and recomputed with __fdiv_rn only when
+// the cheap quotient is ambiguous, so they are bit-identical to encode_scaled
+// (quantize.cpp:19-27).
+#include <cstdint>
+
+#include "coat_device.cuh"
+#include "coat_internal.h"
+
+namespace coat {
+namespace {
+
+constexpr float kRelQ = 0x1p-20f;   // |x*RN(1/s) - x/s| <= 2^-23 relative; 8x margin
+constexpr int kThreads = 256;
+
+struct Chunk16 {
+    float v[16];
+};
+
+template <int DT>  // 0: fp32, 1: bf16
+__device__ __forceinline__ Chunk16 load16(const void* x, int64_t e0) {
+    Chunk16 c;
+    if (DT == 0) {
+        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(x) + e0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float4 a = p[k];
+            c.v[4 * k] = a.x; c.v[4 * k + 1] = a.y; c.v[4 * k + 2] = a.z; c.v[4 * k + 3] = a.w;
+        }
+    } else {
+        const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + e0);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint4 a = p[k];
+            const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                c.v[8 * k + 2 * i] = u2f(w[i] << 16);
+                c.v[8 * k + 2 * i + 1] = u2f(w[i] & 0xFFFF0000u);
+            }
+        }
+    }
+    return c;
+}
+
+template <int DT>
+__device__ __forceinline__ float load1(const void* x, int64_t i) {
+    if (DT == 0) return static_cast<const float*>(x)[i];
+    return u2f(uint32_t(static_cast<const uint16_t*>(x)[i]) << 16);
+}
+
+// |x| bit pattern for a max that ignores NaN like std::max(m, fabs(NaN)) == m
+// (quantize.cpp:104-105 / 137-139); Inf is kept.
+__device__ __forceinline__ uint32_t abs_bits_nan0(float x) {
+    const uint32_t a = f2u(x) & 0x7FFFFFFFu;
+    return a > 0x7F800000u ? 0u : a;
+}
+
+__device__ __forceinline__ uint32_t encode_exact(float x, float s, float inv_s) {
+    uint32_t code;
+    if (certified_code(__fmul_rn(x, inv_s), kRelQ, code)) return code;
+    return e4m3_encode(__fdiv_rn(x, s));
+}
+
+__device__ __forceinline__ uint4 encode16(const Chunk16& c, float s, float inv_s) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        w[k] = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[k] |= encode_exact(c.v[4 * k + i], s, inv_s) << (8 * i);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ---------------------------------------------------------------- per-group --
+// G = 16 * L with L in {1,2,4,8,16,32}: L lanes per group.
+template <int DT, int L>
+__global__ void __launch_bounds__(kThreads)
+quant_group_kernel(const void* __restrict__ x, int64_t nchunks, uint8_t* __restrict__ codes,
+                   uint16_t* __restrict__ scales, uint32_t* flags) {
+    uint32_t bad = 0;
+    const int64_t stride = int64_t(gridDim.x) * kThreads;
+    for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch - threadIdx.x % 32 < nchunks; ch += stride) {
+        // keep whole warps in the loop so the group shuffles stay converged
+        const bool valid = ch < nchunks;
+        Chunk16 c;
+        if (valid) c = load16<DT>(x, ch * 16);
+        uint32_t am = 0;
+        if (valid) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t a = f2u(c.v[i]) & 0x7FFFFFFFu;
+                bad |= a >= 0x7F800000u;
+                am = max(am, a);
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
+        if (valid) {
+            const float s = group_scale(u2f(am));
+            const float inv_s = __frcp_rn(s);
+            reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, inv_s);
+            if ((threadIdx.x % L) == 0) scales[ch / L] = float_to_bf16_bits_exact(s);
+        }
+    }
+    if (flags && __reduce_or_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagNonFiniteInput);
+}
+
+// Generic per-group quantizer for any G (one warp per group, strided).
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+quant_group_generic_kernel(const void* __restrict__ x, int64_t n, int64_t G, uint8_t* __restrict__ codes,
+                           uint16_t* __restrict__ scales, uint32_t* flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ng = n / G;
+    uint32_t bad = 0;
+    for (int64_t grp = (blockIdx.x * int64_t(kThreads) + threadIdx.x) / 32; grp < ng;
+         grp += int64_t(gridDim.x) * kThreads / 32) {
+        uint32_t am = 0;
+        for (int64_t i = lane; i < G; i += 32) {
+            const uint32_t a = f2u(load1<DT>(x, grp * G + i)) & 0x7FFFFFFFu;
+            bad |= a >= 0x7F800000u;
+            am = max(am, a);
+        }
+        am = warp_max_u32(am);
+        const float s = group_scale(u2f(am));
+        const float inv_s = __frcp_rn(s);
+        for (int64_t i = lane; i < G; i += 32)
+            codes[grp * G + i] = (uint8_t)encode_exact(load1<DT>(x, grp * G + i), s, inv_s);
+        if (lane == 0) scales[grp] = float_to_bf16_bits_exact(s);
+    }
+    if (flags && __reduce_or_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, kFlagNonFiniteInput);
+}
+
+// ---------------------------------------------------------------- dequantize --
+// out = decode(code) * scale[i / G]  (quantize.cpp:113-124), fp32 or bf16 out.
+template <int ODT>
+__global__ void __launch_bounds__(kThreads)
+dequant_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ scales, int64_t n,
+               int64_t G, void* __restrict__ out) {
+    const int64_t nchunks = n / 16;
+    const bool chunk_scale = (G % 16) == 0;
+    for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch < nchunks;
+         ch += int64_t(gridDim.x) * kThreads) {
+        const uint4 cw = reinterpret_cast<const uint4*>(codes)[ch];
+        const uint32_t w[4] = {cw.x, cw.y, cw.z, cw.w};
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 a = e4m3x2_decode(w[k] & 0xFFFFu);
+            const float2 b = e4m3x2_decode(w[k] >> 16);
+            v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = b.x; v[4 * k + 3] = b.y;
+        }
+        if (chunk_scale) {
+            const float s = bf16_bits_to_float(scales[ch * 16 / G]);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], s);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], bf16_bits_to_float(scales[(ch * 16 + i) / G]));
+        }
+        if (ODT == 0) {
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + ch * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+            uint32_t p[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                p[k] = (f2u(round_bf16(v[2 * k])) >> 16) | (f2u(round_bf16(v[2 * k + 1])) & 0xFFFF0000u);
+            uint4* o = reinterpret_cast<uint4*>(static_cast<uint16_t*>(out) + ch * 16);
+            o[0] = make_uint4(p[0], p[1], p[2], p[3]);
+            o[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        }
+    }
+    // tail (n % 16)
+    const int64_t t = nchunks * 16 + blockIdx.x * int64_t(kThreads) + threadIdx.x;
+    if (blockIdx.x == 0 && t < n) {
+        const float v = __fmul_rn(e4m3_decode(codes[t]), bf16_bits_to_float(scales[t / G]));
+        if (ODT == 0) static_cast<float*>(out)[t] = v;
+        else static_cast<uint16_t*>(out)[t] = (uint16_t)(f2u(round_bf16(v)) >> 16);
+    }
+}
+
+// ------------------------------------------------- Group Scaling amax (K3) ----
+// Stage 1: per-1xG absmax -> intermediate (optional).  Stage 2: global max via
+// a block max + one atomicMax per CTA on the fp32 bit pattern.
+template <int DT, int L>
+__global__ void __launch_bounds__(kThreads)
+group_amax_kernel(const void* __restrict__ x, int64_t nchunks, float* __restrict__ inter,
+                  uint32_t* global_bits) {
+    __shared__ uint32_t wmax[kThreads / 32];
+    uint32_t gm = 0;
+    for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch - threadIdx.x % 32 < nchunks;
+         ch += int64_t(gridDim.x) * kThreads) {
+        const bool valid = ch < nchunks;
+        uint32_t am = 0;
+        if (valid) {
+            const Chunk16 c = load16<DT>(x, ch * 16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) am = max(am, abs_bits_nan0(c.v[i]));
+        }
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
+        if (valid && inter && (threadIdx.x % L) == 0) inter[ch / L] = u2f(am);
+        gm = max(gm, am);
+    }
+    gm = warp_max_u32(gm);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = gm;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint32_t v = threadIdx.x < kThreads / 32 ? wmax[threadIdx.x] : 0u;
+        v = warp_max_u32(v);
+        if (threadIdx.x == 0 && v) atomicMax(global_bits, v);
+    }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+group_amax_generic_kernel(const void* __restrict__ x, int64_t n, int64_t G, float* __restrict__ inter,
+                          uint32_t* global_bits) {
+    const int lane = threadIdx.x & 31;
+    uint32_t gm = 0;
+    for (int64_t grp = (blockIdx.x * int64_t(kThreads) + threadIdx.x) / 32; grp < n / G;
+         grp += int64_t(gridDim.x) * kThreads / 32) {
+        uint32_t am = 0;
+        for (int64_t i = lane; i < G; i += 32) am = max(am, abs_bits_nan0(load1<DT>(x, grp * G + i)));
+        am = warp_max_u32(am);
+        if (lane == 0 && inter) inter[grp] = u2f(am);
+        gm = max(gm, am);
+    }
+    if (lane == 0 && gm) atomicMax(global_bits, gm);
+}
+
+// --------------------------------------------------------- per-tensor (K3) ----
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+quant_tensor_kernel(const void* __restrict__ x, int64_t n, const uint32_t* amax_bits,
+                    uint8_t* __restrict__ codes, uint16_t* scale_out, uint32_t* flags) {
+    const float s = group_scale(u2f(*amax_bits));
+    const float inv_s = __frcp_rn(s);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && scale_out) *scale_out = float_to_bf16_bits_exact(s);
+    uint32_t bad = 0;
+    const int64_t nchunks = n / 16;
+    for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch < nchunks;
+         ch += int64_t(gridDim.x) * kThreads) {
+        const Chunk16 c = load16<DT>(x, ch * 16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) bad |= (f2u(c.v[i]) & 0x7FFFFFFFu) >= 0x7F800000u;
+        reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, inv_s);
+    }
+    const int64_t t = nchunks * 16 + blockIdx.x * int64_t(kThreads) + threadIdx.x;
+    if (blockIdx.x == 0 && t < n) {
+        const float v = load1<DT>(x, t);
+        bad |= (f2u(v) & 0x7FFFFFFFu) >= 0x7F800000u;
+        codes[t] = (uint8_t)encode_exact(v, s, inv_s);
+    }
+    if (flags && __reduce_or_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagNonFiniteInput);
+}
+
+// ------------------------------------------------------------- flat codec ----
+__global__ void encode_kernel(const float* __restrict__ x, uint8_t* __restrict__ out, int64_t n, uint32_t* flags) {
+    uint32_t bad = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float v = x[i];
+        bad |= (f2u(v) & 0x7FFFFFFFu) >= 0x7F800000u;
+        out[i] = (uint8_t)e4m3_encode(v);
+    }
+    if (flags && bad) atomicOr(flags, kFlagNonFiniteInput);
+}
+
+__global__ void decode_kernel(const uint8_t* __restrict__ c, float* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = e4m3_decode(c[i]);
+}
+
+int blocks_for(int64_t work_items) {
+    const int64_t cap = int64_t(device_sm_count()) * 8;   // 8 CTAs x 256 thr = 64 warps/SM
+    return (int)imax64(1, imin64((work_items + kThreads - 1) / kThreads, cap));
+}
+
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers --
+cudaError_t launch_encode_e4m3(const float* x, uint8_t* out, int64_t n, uint32_t* flags, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    encode_kernel<<<blocks_for(n), kThreads, 0, st>>>(x, out, n, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_e4m3(const uint8_t* codes, float* out, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    decode_kernel<<<blocks_for(n), kThreads, 0, st>>>(codes, out, n);
+    return cudaGetLastError();
+}
+
+#define COAT_GROUP_SWITCH(L_EXPR, CALL)                 \
+    switch (L_EXPR) {                                   \
+        case 1: { constexpr int L = 1; CALL; } break;   \
+        case 2: { constexpr int L = 2; CALL; } break;   \
+        case 4: { constexpr int L = 4; CALL; } break;   \
+        case 8: { constexpr int L = 8; CALL; } break;   \
+        case 16: { constexpr int L = 16; CALL; } break; \
+        case 32: { constexpr int L = 32; CALL; } break; \
+        default: break;                                 \
+    }
+
+static bool pow2_lanes(int64_t G, int* L) {
+    if (G % 16 != 0) return false;
+    const int64_t l = G / 16;
+    if (l > 32 || (l & (l - 1)) != 0) return false;
+    *L = (int)l;
+    return true;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+cudaError_t launch_quantize_per_group(const void* x, int dtype, int64_t n, int64_t G, uint8_t* codes,
+                                      uint16_t* scales, uint32_t* flags, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int L = 0;
+    if (pow2_lanes(G, &L) && aligned16(x) && aligned16(codes)) {
+        const int64_t nchunks = n / 16;
+        if (dtype == 0) {
+            COAT_GROUP_SWITCH(L, (quant_group_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, codes, scales, flags)));
+        } else {
+            COAT_GROUP_SWITCH(L, (quant_group_kernel<1, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, codes, scales, flags)));
+        }
+    } else {
+        const int64_t warps = n / G;
+        const int blocks = blocks_for(warps * 32);
+        if (dtype == 0) quant_group_generic_kernel<0><<<blocks, kThreads, 0, st>>>(x, n, G, codes, scales, flags);
+        else quant_group_generic_kernel<1><<<blocks, kThreads, 0, st>>>(x, n, G, codes, scales, flags);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_per_group(const uint8_t* codes, const uint16_t* scales, int64_t n, int64_t G,
+                                        void* out, int out_dtype, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (!aligned16(codes) || !aligned16(out)) return cudaErrorMisalignedAddress;
+    const int blocks = blocks_for(imax64(n / 16, 1));
+    if (out_dtype == 0) dequant_kernel<0><<<blocks, kThreads, 0, st>>>(codes, scales, n, G, out);
+    else dequant_kernel<1><<<blocks, kThreads, 0, st>>>(codes, scales, n, G, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_group_amax(const void* x, int dtype, int64_t n, int64_t G, float* inter,
+                              uint32_t* global_bits, uint32_t* flags, cudaStream_t st) {
+    (void)flags;
+    cudaError_t e = cudaMemsetAsync(global_bits, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess || n <= 0) return e;
+    int L = 0;
+    if (pow2_lanes(G, &L) && aligned16(x)) {
+        const int64_t nchunks = n / 16;
+        if (dtype == 0) {
+            COAT_GROUP_SWITCH(L, (group_amax_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, inter, global_bits)));
+        } else {
+            COAT_GROUP_SWITCH(L, (group_amax_kernel<1, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, inter, global_bits)));
+        }
+    } else {
+        const int blocks = blocks_for((n / G) * 32);
+        if (dtype == 0) group_amax_generic_kernel<0><<<blocks, kThreads, 0, st>>>(x, n, G, inter, global_bits);
+        else group_amax_generic_kernel<1><<<blocks, kThreads, 0, st>>>(x, n, G, inter, global_bits);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_per_tensor(const void* x, int dtype, int64_t n, const uint32_t* amax_bits,
+                                       uint8_t* codes, uint16_t* scale_out, uint32_t* flags, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (!aligned16(x) || !aligned16(codes)) return cudaErrorMisalignedAddress;
+    const int blocks = blocks_for(imax64(n / 16, 1));
+    if (dtype == 0) quant_tensor_kernel<0><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags);
+    else quant_tensor_kernel<1><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags);
+    return cudaGetLastError();
+}
+
+}  // namespace coat

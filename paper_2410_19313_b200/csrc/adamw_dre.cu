@@ -1,0 +1,431 @@
+// adamw_dre.cu -- K1: the fused FP8-DRE AdamW step, plus the standalone DRE
+// quantize / contract kernels that share its device code.
+//
+// Reference: coatsim::step (proj/core/src/optimizer.cpp:101-114) with the
+// policy {E4M3, expand=true, G=128} for both moments:
+//   m,v = unpack_moment(slot)            optimizer.cpp:49-55  (dequantize + contract)
+//   adamw_update(w, m, v, g, t)          optimizer.cpp:57-68  (fp32, no FMA)
+//   slot.m/v = pack_moment(m/v)          optimizer.cpp:40-47  (measure, expand, quantize)
+// The reference makes ~10 full passes over memory; this kernel makes one:
+// it reads w, g, the two code arrays and the per-group {scale, k, c}, and
+// writes w, the new codes and the new per-group {scale, k, c}:
+//   16 B/param (w r/w 8, g 4, codes r/w 2x2) + 40 B per 128-group of metadata
+//   = 16.3125 B/param of compulsory HBM traffic.
+//
+// Work decomposition (B200): one warp owns a "tile" of 4 groups = 512
+// params; lane l holds params 4l..4l+3 of every group, so every global access
+// is a fully-coalesced 128-bit (w, g) or 32-bit (codes) warp-contiguous load.
+// Group extrema are single redux.sync instructions on the fp32 bit patterns
+// (non-negative floats order like u32).  The 8 (group, moment) parameter sets
+// of a tile (k, c, scale -- double-precision log/sqrt/pow as in the
+// reference) are computed by 8 lanes in one pass and shared through shared
+// memory.  Grid = a persistent multiple of the SM count.
+//
+// Error semantics (errors.hpp:8-22): non-finite gradients set
+// kFlagNonFiniteGrad; a moment whose expanded values are not finite sets
+// kFlagPackM / kFlagPackV.  The state is written to SEPARATE output buffers
+// (ping-pong), so the host commits exactly what the reference would have
+// committed (see paper_2410_19313_b200/coatsim.py: step()).
+#include <cstdint>
+
+#include "coat_device.cuh"
+#include "dre.cuh"
+#include "coat_internal.h"
+
+namespace coat {
+namespace {
+
+using dre::ContractParams;
+using dre::PackParams;
+
+constexpr int kTileGroups = 4;
+constexpr int kTile = kTileGroups * dre::kG;   // 512 params per warp tile
+constexpr int kWarps = 8;                      // warps per CTA
+constexpr int kThreads = kWarps * 32;
+
+struct StepScalars {
+    float b1, b2, omb1, omb2, lr, wd, eps, bc1, bc2;
+    double log_target;
+};
+
+struct WarpShared {
+    ContractParams cp[8];   // [moment*4 + group] of the incoming state
+    PackParams pp[8];       // [moment*4 + group] of the outgoing state
+    uint32_t ext[16];       // lo/hi bit patterns per pair
+};
+
+// Load the incoming per-group meta for pair p = mom*4+grp (lanes 0..7).
+__device__ __forceinline__ ContractParams load_contract(const MomentStateIn& st, int64_t grp) {
+    const float s = bf16_bits_to_float(st.scales[grp]);
+    return dre::contract_prepare(s, st.k[grp], st.c[grp]);
+}
+
+__device__ __forceinline__ void store_pack(const MomentStateOut& st, int64_t grp, const PackParams& p) {
+    st.scales[grp] = float_to_bf16_bits_exact(p.s);
+    st.k[grp] = p.k;
+    st.c[grp] = p.c;
+}
+
+// AdamW on one element, bit-identical to adamw_update (optimizer.cpp:57-68).
+__device__ __forceinline__ void adamw_one(float& w, float& m, float& v, float g, const StepScalars& S) {
+    m = __fadd_rn(__fmul_rn(S.b1, m), __fmul_rn(S.omb1, g));
+    v = __fadd_rn(__fmul_rn(S.b2, v), __fmul_rn(S.omb2, __fmul_rn(g, g)));
+    const float mhat = __fdiv_rn(m, S.bc1);
+    const float vhat = __fdiv_rn(v, S.bc2);
+    const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), S.eps)), __fmul_rn(S.wd, w));
+    w = __fsub_rn(w, __fmul_rn(S.lr, upd));
+}
+
+// Exact extrema of |x| over nonzero elements; NaN/Inf map above every finite.
+__device__ __forceinline__ void extrema4(const float (&x)[4], uint32_t& lo, uint32_t& hi) {
+    lo = 0xFFFFFFFFu;
+    hi = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t a = f2u(x[i]) & 0x7FFFFFFFu;
+        hi = max(hi, a);
+        lo = min(lo, a == 0u ? 0xFFFFFFFFu : a);
+    }
+}
+
+// Compute pack params for the pairs of this warp from their extrema held in
+// ws.ext (lane p < npairs works on pair p), publish through ws.pp.
+__device__ __forceinline__ void pack_params_pass(WarpShared& ws, int lane, int npairs, double log_target) {
+    if (lane < npairs) {
+        const uint32_t lo = ws.ext[2 * lane], hi = ws.ext[2 * lane + 1];
+        PackParams p;
+        if (hi >= 0x7F800000u) {               // non-finite moment value
+            p = dre::pack_prepare(1.0f, 1.0f, log_target);
+            p.bad = true;
+            p.mode = 2;
+        } else {
+            p = dre::pack_prepare(u2f(lo), u2f(hi), log_target);
+        }
+        ws.pp[lane] = p;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ uint32_t pack4(const float (&x)[4], const PackParams& p, uint32_t& fb) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c |= dre::pack_one(x[i], p, fb) << (8 * i);
+    return c;
+}
+
+__device__ __forceinline__ void contract4(uint32_t codes, const ContractParams& p, float (&x)[4], bool& bad) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = dre::contract_one((codes >> (8 * i)) & 0xFFu, p, bad);
+}
+
+// ----------------------------------------------------------------------------
+// K1: fused step.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+adamw_dre_step_kernel(const float* w_in, float* w_out, const float* __restrict__ g, int64_t n,
+                      MomentStateIn m_in, MomentStateIn v_in, MomentStateOut m_out,
+                      MomentStateOut v_out, StepScalars S, uint32_t* flags,
+                      unsigned long long* fallback_counter) {
+    __shared__ WarpShared shared[kWarps];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    WarpShared& ws = shared[wid];
+    const int64_t ng = (n + dre::kG - 1) / dre::kG;
+    const int64_t ntiles = (ng + kTileGroups - 1) / kTileGroups;
+    const int64_t warp_global = int64_t(blockIdx.x) * kWarps + wid;
+    const int64_t warp_stride = int64_t(gridDim.x) * kWarps;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(w_in) | reinterpret_cast<uintptr_t>(w_out) |
+                          reinterpret_cast<uintptr_t>(g)) & 15u) == 0;
+    uint32_t myflags = 0;
+    uint32_t fallbacks = 0;
+
+    for (int64_t tile = warp_global; tile < ntiles; tile += warp_stride) {
+        const int64_t g0 = tile * kTileGroups;
+        const int gvalid = (int)imin64(kTileGroups, ng - g0);
+        const int64_t base = g0 * dre::kG;
+        const bool full = vec_ok && base + kTile <= n;
+
+        // ---- incoming per-group meta: lane p = mom*4 + grp
+        if (lane < 8) {
+            const int mom = lane >> 2, grp = lane & 3;
+            if (grp < gvalid) ws.cp[lane] = load_contract(mom ? v_in : m_in, g0 + grp);
+        }
+        // ---- streaming loads
+        float w[kTileGroups][4], gr[kTileGroups][4];
+        uint32_t cm[kTileGroups], cv[kTileGroups];
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j) {
+            const int64_t e0 = base + j * dre::kG + 4 * lane;
+            if (j < gvalid) {
+                cm[j] = ldg_u32(m_in.codes + e0);
+                cv[j] = ldg_u32(v_in.codes + e0);
+            } else {
+                cm[j] = cv[j] = 0u;
+            }
+            if (full) {
+                const float4 a = ldg_f4(w_in + e0);
+                const float4 b = ldg_stream_f4(g + e0);
+                w[j][0] = a.x; w[j][1] = a.y; w[j][2] = a.z; w[j][3] = a.w;
+                gr[j][0] = b.x; gr[j][1] = b.y; gr[j][2] = b.z; gr[j][3] = b.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool in = e0 + i < n;
+                    w[j][i] = in ? w_in[e0 + i] : 0.0f;
+                    gr[j][i] = in ? g[e0 + i] : 0.0f;
+                }
+            }
+        }
+        __syncwarp();
+
+        // ---- unpack (dequantize + contract) and AdamW
+        float m[kTileGroups][4], v[kTileGroups][4];
+        bool bad_state = false;
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j) {
+            if (j < gvalid) {
+                contract4(cm[j], ws.cp[j], m[j], bad_state);
+                contract4(cv[j], ws.cp[4 + j], v[j], bad_state);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) m[j][i] = v[j][i] = 0.0f;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (!isfinite(gr[j][i])) myflags |= kFlagNonFiniteGrad;
+                adamw_one(w[j][i], m[j][i], v[j][i], gr[j][i], S);
+                if (base + j * dre::kG + 4 * lane + i >= n) m[j][i] = v[j][i] = 0.0f;  // pad_flat
+            }
+        }
+        if (bad_state) myflags |= kFlagContract;
+
+        // ---- group extrema (exact) for both moments: 16 redux.sync
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j) {
+            uint32_t l, h;
+            extrema4(m[j], l, h);
+            lo[j] = warp_min_u32(l);
+            hi[j] = warp_max_u32(h);
+            extrema4(v[j], l, h);
+            lo[4 + j] = warp_min_u32(l);
+            hi[4 + j] = warp_max_u32(h);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                ws.ext[2 * p] = lo[p];
+                ws.ext[2 * p + 1] = hi[p];
+            }
+        }
+        __syncwarp();
+        pack_params_pass(ws, lane, 8, S.log_target);
+
+        // ---- outgoing meta (lanes 0..7) + codes + weights
+        if (lane < 8) {
+            const int mom = lane >> 2, grp = lane & 3;
+            if (grp < gvalid) {
+                const PackParams& p = ws.pp[lane];
+                store_pack(mom ? v_out : m_out, g0 + grp, p);
+                if (p.bad) myflags |= mom ? kFlagPackV : kFlagPackM;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j) {
+            const int64_t e0 = base + j * dre::kG + 4 * lane;
+            if (j < gvalid) {
+                stg_u32(m_out.codes + e0, pack4(m[j], ws.pp[j], fallbacks));
+                stg_u32(v_out.codes + e0, pack4(v[j], ws.pp[4 + j], fallbacks));
+            }
+            if (full) {
+                stg_stream_f4(w_out + e0, make_float4(w[j][0], w[j][1], w[j][2], w[j][3]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (e0 + i < n) w_out[e0 + i] = w[j][i];
+            }
+        }
+        __syncwarp();
+    }
+    myflags = warp_or_u32(myflags);
+    if (lane == 0 && myflags && flags) atomicOr(flags, myflags);
+    if (fallback_counter) {
+        const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, fallbacks);
+        if (lane == 0 && tot) atomicAdd(fallback_counter, (unsigned long long)tot);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// expand_quantize (expand.cpp:115-135) of a flat fp32 tensor, n % 128 == 0.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+expand_quantize_kernel(const float* __restrict__ x, int64_t n, MomentStateOut out, double log_target,
+                       uint32_t* flags, unsigned long long* fallback_counter) {
+    __shared__ WarpShared shared[kWarps];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    WarpShared& ws = shared[wid];
+    const int64_t ng = n / dre::kG;
+    const int64_t ntiles = (ng + kTileGroups - 1) / kTileGroups;
+    uint32_t myflags = 0, fallbacks = 0;
+    for (int64_t tile = int64_t(blockIdx.x) * kWarps + wid; tile < ntiles;
+         tile += int64_t(gridDim.x) * kWarps) {
+        const int64_t g0 = tile * kTileGroups;
+        const int gvalid = (int)imin64(kTileGroups, ng - g0);
+        const int64_t base = g0 * dre::kG;
+        float xv[kTileGroups][4];
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j) {
+            if (j < gvalid) {
+                const float4 a = ldg_stream_f4(x + base + j * dre::kG + 4 * lane);
+                xv[j][0] = a.x; xv[j][1] = a.y; xv[j][2] = a.z; xv[j][3] = a.w;
+            } else {
+                xv[j][0] = xv[j][1] = xv[j][2] = xv[j][3] = 0.0f;
+            }
+        }
+        uint32_t lo[4], hi[4];
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j) {
+            uint32_t l, h;
+            extrema4(xv[j], l, h);
+            lo[j] = warp_min_u32(l);
+            hi[j] = warp_max_u32(h);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                ws.ext[2 * p] = lo[p];
+                ws.ext[2 * p + 1] = hi[p];
+            }
+        }
+        __syncwarp();
+        pack_params_pass(ws, lane, 4, log_target);
+        if (lane < gvalid) {
+            store_pack(out, g0 + lane, ws.pp[lane]);
+            if (ws.pp[lane].bad) myflags |= kFlagNonFiniteInput;
+        }
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j)
+            if (j < gvalid) stg_u32(out.codes + base + j * dre::kG + 4 * lane, pack4(xv[j], ws.pp[j], fallbacks));
+        __syncwarp();
+    }
+    myflags = warp_or_u32(myflags);
+    if (lane == 0 && myflags && flags) atomicOr(flags, myflags);
+    if (fallback_counter) {
+        const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, fallbacks);
+        if (lane == 0 && tot) atomicAdd(fallback_counter, (unsigned long long)tot);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// dequantize_contract (expand.cpp:137-141), n % 128 == 0.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+dequantize_contract_kernel(MomentStateIn in, int64_t n, float* __restrict__ x, uint32_t* flags) {
+    __shared__ WarpShared shared[kWarps];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    WarpShared& ws = shared[wid];
+    const int64_t ng = n / dre::kG;
+    const int64_t ntiles = (ng + kTileGroups - 1) / kTileGroups;
+    bool bad = false;
+    for (int64_t tile = int64_t(blockIdx.x) * kWarps + wid; tile < ntiles;
+         tile += int64_t(gridDim.x) * kWarps) {
+        const int64_t g0 = tile * kTileGroups;
+        const int gvalid = (int)imin64(kTileGroups, ng - g0);
+        const int64_t base = g0 * dre::kG;
+        if (lane < gvalid) ws.cp[lane] = load_contract(in, g0 + lane);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kTileGroups; ++j) {
+            if (j < gvalid) {
+                const int64_t e0 = base + j * dre::kG + 4 * lane;
+                float v[4];
+                contract4(ldg_u32(in.codes + e0), ws.cp[j], v, bad);
+                stg_stream_f4(x + e0, make_float4(v[0], v[1], v[2], v[3]));
+            }
+        }
+        __syncwarp();
+    }
+    if (flags && warp_or_u32(bad ? 1u : 0u) && lane == 0) atomicOr(flags, kFlagContract | kFlagNonFiniteInput);
+}
+
+// make_slot (optimizer.cpp:90-99): every group degenerate, k = c = 1,
+// scale = round_bf16(2^-9) = 2^-9, codes 0.
+__global__ void make_slot_kernel(MomentStateOut st, int64_t npad) {
+    const int64_t ng = npad / dre::kG;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npad / 16;
+         i += int64_t(gridDim.x) * blockDim.x)
+        reinterpret_cast<uint4*>(st.codes)[i] = make_uint4(0, 0, 0, 0);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ng;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        st.scales[i] = 0x3B00u;   // bf16(2^-9)
+        st.k[i] = 1.0f;
+        st.c[i] = 1.0f;
+    }
+}
+
+int grid_for(int64_t tiles, int per_cta) {
+    const int sms = device_sm_count();
+    const int64_t want = (tiles + per_cta - 1) / per_cta;
+    const int64_t cap = int64_t(sms) * 4;   // persistent: 4 CTAs (32 warps) per SM
+    return (int)imax64(1, imin64(want, cap));
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// host launchers (called by the C-ABI in api.cu)
+// ----------------------------------------------------------------------------
+cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n,
+                                  const MomentStateIn& m_in, const MomentStateIn& v_in,
+                                  const MomentStateOut& m_out, const MomentStateOut& v_out,
+                                  const AdamWScalars& a, uint32_t* flags,
+                                  unsigned long long* fallbacks, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    StepScalars S;
+    S.b1 = a.beta1;
+    S.b2 = a.beta2;
+    S.omb1 = 1.0f - a.beta1;
+    S.omb2 = 1.0f - a.beta2;
+    S.lr = a.lr;
+    S.wd = a.weight_decay;
+    S.eps = a.eps;
+    S.bc1 = a.bc1;
+    S.bc2 = a.bc2;
+    S.log_target = a.log_target;
+    const int64_t ng = (n + dre::kG - 1) / dre::kG;
+    const int64_t ntiles = (ng + kTileGroups - 1) / kTileGroups;
+    adamw_dre_step_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(
+        w_in, w_out, g, n, m_in, v_in, m_out, v_out, S, flags, fallbacks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand_quantize(const float* x, int64_t n, const MomentStateOut& out,
+                                   double log_target, uint32_t* flags,
+                                   unsigned long long* fallbacks, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t ntiles = (n / dre::kG + kTileGroups - 1) / kTileGroups;
+    expand_quantize_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(x, n, out, log_target,
+                                                                               flags, fallbacks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_contract(const MomentStateIn& in, int64_t n, float* x, uint32_t* flags,
+                                       cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t ntiles = (n / dre::kG + kTileGroups - 1) / kTileGroups;
+    dequantize_contract_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(in, n, x, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_make_slot(const MomentStateOut& st, int64_t npad, cudaStream_t stream) {
+    if (npad <= 0) return cudaSuccess;
+    const int threads = 256;
+    const int64_t work = imax64(npad / 16, npad / dre::kG);
+    const int blocks = (int)imin64((work + threads - 1) / threads, int64_t(device_sm_count()) * 8);
+    make_slot_kernel<<<max(blocks, 1), threads, 0, stream>>>(st, npad);
+    return cudaGetLastError();
+}
+
+}  // namespace coat

@@ -1,0 +1,206 @@
+// api.cu -- the extern "C" boundary (include/coat.h) over the sm_100a kernels.
+// Host-side validation mirrors the reference's synchronous exceptions
+// (GeometryMismatch / ShapeMismatch / InvalidSpec are thrown before any work,
+// e.g. quantize.cpp:38-57, optimizer.cpp:102-103); data-dependent errors are
+// reported through the device flag word.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/coat.h"
+#include "coat_internal.h"
+
+namespace coat {
+
+static thread_local char g_last_error[256] = "";
+static unsigned long long* g_fallback_counter = nullptr;
+
+int device_sm_count() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static int cached[64] = {0};
+    if (dev < 0 || dev >= 64) return 148;
+    if (cached[dev] == 0) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = sms > 0 ? sms : 148;
+    }
+    return cached[dev];
+}
+
+static coat_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return COAT_OK;
+    std::snprintf(g_last_error, sizeof(g_last_error), "CUDA: %s", cudaGetErrorString(e));
+    return COAT_ERR_CUDA;
+}
+
+static coat_status fail(coat_status s, const char* msg) {
+    std::snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
+    return s;
+}
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static MomentStateIn in_of(const coat_moment_state& s) { return {s.codes, s.scales, s.k, s.c}; }
+static MomentStateOut out_of(const coat_moment_state& s) { return {s.codes, s.scales, s.k, s.c}; }
+static bool state_ok(const coat_moment_state& s) {
+    return s.codes && s.scales && s.k && s.c && (reinterpret_cast<uintptr_t>(s.codes) & 15u) == 0;
+}
+
+}  // namespace coat
+
+using namespace coat;
+
+extern "C" {
+
+const char* coat_version(void) { return "coat-b200 0.1.0 (sm_100a)"; }
+
+const char* coat_status_string(coat_status s) {
+    switch (s) {
+        case COAT_OK: return "ok";
+        case COAT_ERR_SHAPE: return "ShapeMismatch";
+        case COAT_ERR_GEOMETRY: return "GeometryMismatch";
+        case COAT_ERR_NONFINITE_INPUT: return "NonFiniteInput";
+        case COAT_ERR_NONFINITE_GRAD: return "NonFiniteGradient";
+        case COAT_ERR_INVALID: return "InvalidSpec";
+        case COAT_ERR_CUDA: return "CudaError";
+        case COAT_ERR_NCCL: return "NcclError";
+        case COAT_ERR_OUT_OF_RANGE: return "OutOfRange";
+        case COAT_ERR_ALL_ZERO_GROUP: return "AllZeroGroup";
+        case COAT_ERR_IO: return "IoError";
+        case COAT_ERR_BAD_MAGIC: return "BadMagic";
+    }
+    return "unknown";
+}
+
+const char* coat_last_error(void) { return g_last_error; }
+
+coat_status coat_flags_to_status(uint32_t flags) {
+    if (flags & COAT_FLAG_NONFINITE_GRAD) return COAT_ERR_NONFINITE_GRAD;  // checked first, optimizer.cpp:104
+    if (flags & (COAT_FLAG_NONFINITE_INPUT | COAT_FLAG_PACK_M | COAT_FLAG_PACK_V | COAT_FLAG_CONTRACT))
+        return COAT_ERR_NONFINITE_INPUT;
+    return COAT_OK;
+}
+
+int coat_device_sm_count(void) { return device_sm_count(); }
+
+coat_status coat_set_fallback_counter(unsigned long long* d_counter) {
+    g_fallback_counter = d_counter;
+    return COAT_OK;
+}
+
+// ------------------------------------------------------------------ codec --
+coat_status coat_encode_e4m3(const float* x, uint8_t* codes, int64_t n, uint32_t* d_flags, void* stream) {
+    if (n < 0) return fail(COAT_ERR_INVALID, "encode: negative n");
+    return cuda_status(launch_encode_e4m3(x, codes, n, d_flags, S(stream)));
+}
+
+coat_status coat_decode_e4m3(const uint8_t* codes, float* x, int64_t n, void* stream) {
+    if (n < 0) return fail(COAT_ERR_INVALID, "decode: negative n");
+    return cuda_status(launch_decode_e4m3(codes, x, n, S(stream)));
+}
+
+// -------------------------------------------------------------- quantizer --
+static coat_status check_group(int64_t rows, int64_t cols, int64_t G, int dtype) {
+    if (rows <= 0 || cols <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (dtype != 0 && dtype != 1) return fail(COAT_ERR_INVALID, "dtype must be 0 (fp32) or 1 (bf16)");
+    if (G <= 0) return fail(COAT_ERR_GEOMETRY, "per-group: group size must be positive");
+    if (cols % G != 0) return fail(COAT_ERR_GEOMETRY, "per-group: last dim not divisible by group size");
+    return COAT_OK;
+}
+
+coat_status coat_quantize_per_group(const void* x, int dtype, int64_t rows, int64_t cols, int64_t G,
+                                    uint8_t* codes, uint16_t* scales, uint32_t* d_flags, void* stream) {
+    const coat_status st = check_group(rows, cols, G, dtype);
+    if (st != COAT_OK) return st;
+    return cuda_status(launch_quantize_per_group(x, dtype, rows * cols, G, codes, scales, d_flags, S(stream)));
+}
+
+coat_status coat_dequantize_per_group(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,
+                                      int64_t G, void* out, int out_dtype, void* stream) {
+    const coat_status st = check_group(rows, cols, G, out_dtype);
+    if (st != COAT_OK) return st;
+    return cuda_status(launch_dequantize_per_group(codes, scales, rows * cols, G, out, out_dtype, S(stream)));
+}
+
+coat_status coat_group_scale_max(const void* x, int dtype, int64_t rows, int64_t cols, int64_t G,
+                                 float* intermediate, uint32_t* d_amax_bits, void* stream) {
+    const coat_status st = check_group(rows, cols, G, dtype);
+    if (st != COAT_OK) return st;
+    if (!d_amax_bits) return fail(COAT_ERR_INVALID, "group_scale_max: d_amax_bits is NULL");
+    return cuda_status(launch_group_amax(x, dtype, rows * cols, G, intermediate, d_amax_bits, nullptr, S(stream)));
+}
+
+coat_status coat_quantize_per_tensor(const void* x, int dtype, int64_t n, const uint32_t* d_amax_bits,
+                                     uint8_t* codes, uint16_t* d_scale, uint32_t* d_flags, void* stream) {
+    if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (dtype != 0 && dtype != 1) return fail(COAT_ERR_INVALID, "dtype must be 0 (fp32) or 1 (bf16)");
+    if (!d_amax_bits) return fail(COAT_ERR_INVALID, "quantize_per_tensor: d_amax_bits is NULL");
+    return cuda_status(launch_quantize_per_tensor(x, dtype, n, d_amax_bits, codes, d_scale, d_flags, S(stream)));
+}
+
+coat_status coat_dequantize_per_tensor(const uint8_t* codes, const uint16_t* d_scale, int64_t n, void* out,
+                                       int out_dtype, void* stream) {
+    if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (out_dtype != 0 && out_dtype != 1) return fail(COAT_ERR_INVALID, "dtype must be 0 (fp32) or 1 (bf16)");
+    return cuda_status(launch_dequantize_per_group(codes, d_scale, n, n, out, out_dtype, S(stream)));
+}
+
+// ------------------------------------------------------------------ DRE -----
+static const double kLogTarget = std::log(229376.0);  // expand.cpp:52 log(target_range)
+
+coat_status coat_expand_quantize(const float* x, int64_t n, int64_t G, coat_moment_state out, uint32_t* d_flags,
+                                 void* stream) {
+    if (G <= 0 || n % G != 0) return fail(COAT_ERR_GEOMETRY, "expand: numel not divisible by group size");
+    if (G != 128) return fail(COAT_ERR_INVALID, "expand_quantize: only G = 128 is implemented on B200");
+    if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (!state_ok(out) || (reinterpret_cast<uintptr_t>(x) & 15u)) return fail(COAT_ERR_INVALID, "misaligned or NULL buffer");
+    return cuda_status(launch_expand_quantize(x, n, out_of(out), kLogTarget, d_flags, g_fallback_counter, S(stream)));
+}
+
+coat_status coat_dequantize_contract(coat_moment_state in, int64_t n, int64_t G, float* x, uint32_t* d_flags,
+                                     void* stream) {
+    if (G <= 0 || n % G != 0) return fail(COAT_ERR_GEOMETRY, "expand: numel not divisible by group size");
+    if (G != 128) return fail(COAT_ERR_INVALID, "dequantize_contract: only G = 128 is implemented on B200");
+    if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (!state_ok(in) || (reinterpret_cast<uintptr_t>(x) & 15u)) return fail(COAT_ERR_INVALID, "misaligned or NULL buffer");
+    return cuda_status(launch_dequantize_contract(in_of(in), n, x, d_flags, S(stream)));
+}
+
+// ------------------------------------------------------------ optimizer -----
+coat_status coat_make_slot(int64_t n, int64_t G, coat_moment_state m, coat_moment_state v, void* stream) {
+    if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (G != 128) return fail(COAT_ERR_INVALID, "make_slot: only G = 128 is implemented on B200");
+    if (!state_ok(m) || !state_ok(v)) return fail(COAT_ERR_INVALID, "misaligned or NULL state buffer");
+    const int64_t npad = (n + G - 1) / G * G;
+    cudaError_t e = launch_make_slot(out_of(m), npad, S(stream));
+    if (e == cudaSuccess) e = launch_make_slot(out_of(v), npad, S(stream));
+    return cuda_status(e);
+}
+
+coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n, int64_t G,
+                                coat_moment_state m_in, coat_moment_state v_in, coat_moment_state m_out,
+                                coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t,
+                                uint32_t* d_flags, void* stream) {
+    if (!cfg) return fail(COAT_ERR_INVALID, "step: cfg is NULL");
+    if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (G != 128) return fail(COAT_ERR_INVALID, "step: only G = 128 is implemented on B200");
+    if (t < 1) return fail(COAT_ERR_INVALID, "step: t is the 1-based step number");
+    if (!w_in || !w_out || !g) return fail(COAT_ERR_INVALID, "step: NULL buffer");
+    if (!state_ok(m_in) || !state_ok(v_in) || !state_ok(m_out) || !state_ok(v_out))
+        return fail(COAT_ERR_INVALID, "step: misaligned or NULL state buffer");
+    AdamWScalars a;
+    a.beta1 = cfg->beta1;
+    a.beta2 = cfg->beta2;
+    a.lr = cfg->lr;
+    a.weight_decay = cfg->weight_decay;
+    a.eps = cfg->eps;
+    // optimizer.cpp:58-59: float std::pow on the host, exactly as the reference.
+    a.bc1 = 1.0f - std::pow(cfg->beta1, float(t));
+    a.bc2 = 1.0f - std::pow(cfg->beta2, float(t));
+    a.log_target = kLogTarget;
+    return cuda_status(launch_adamw_dre_step(w_in, w_out, g, n, in_of(m_in), in_of(v_in), out_of(m_out),
+                                             out_of(v_out), a, d_flags, g_fallback_counter, S(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// coat_internal.h -- host-side declarations shared by the .cu translation units
+// (not part of the public C-ABI; see include/coat.h for that).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace coat {
+
+struct MomentStateIn {
+    const uint8_t* codes;     // [npad]
+    const uint16_t* scales;   // [npad/128], BF16 bit patterns (scales are BF16-valued)
+    const float* k;           // [npad/128]
+    const float* c;           // [npad/128]
+};
+
+struct MomentStateOut {
+    uint8_t* codes;
+    uint16_t* scales;
+    float* k;
+    float* c;
+};
+
+struct AdamWScalars {
+    float beta1, beta2, lr, weight_decay, eps;
+    float bc1, bc2;           // 1 - powf(beta, t), computed on the host like optimizer.cpp:58-59
+    double log_target;        // log(229376.0), expand.cpp:52
+};
+
+int device_sm_count();
+
+cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n,
+                                  const MomentStateIn& m_in, const MomentStateIn& v_in,
+                                  const MomentStateOut& m_out, const MomentStateOut& v_out,
+                                  const AdamWScalars& a, uint32_t* flags,
+                                  unsigned long long* fallbacks, cudaStream_t stream);
+cudaError_t launch_expand_quantize(const float* x, int64_t n, const MomentStateOut& out,
+                                   double log_target, uint32_t* flags,
+                                   unsigned long long* fallbacks, cudaStream_t stream);
+cudaError_t launch_dequantize_contract(const MomentStateIn& in, int64_t n, float* x,
+                                       uint32_t* flags, cudaStream_t stream);
+cudaError_t launch_make_slot(const MomentStateOut& st, int64_t npad, cudaStream_t stream);
+
+// activation quantizers (act_quant.cu)
+cudaError_t launch_encode_e4m3(const float* x, uint8_t* out, int64_t n, uint32_t* flags,
+                               cudaStream_t stream);
+cudaError_t launch_decode_e4m3(const uint8_t* codes, float* out, int64_t n, cudaStream_t stream);
+cudaError_t launch_quantize_per_group(const void* x, int dtype, int64_t n, int64_t G,
+                                      uint8_t* codes, uint16_t* scales, uint32_t* flags,
+                                      cudaStream_t stream);
+cudaError_t launch_dequantize_per_group(const uint8_t* codes, const uint16_t* scales, int64_t n,
+                                        int64_t G, void* out, int out_dtype, cudaStream_t stream);
+cudaError_t launch_group_amax(const void* x, int dtype, int64_t n, int64_t G, float* intermediate,
+                              uint32_t* global_bits, uint32_t* flags, cudaStream_t stream);
+cudaError_t launch_quantize_per_tensor(const void* x, int dtype, int64_t n,
+                                       const uint32_t* amax_bits, uint8_t* codes,
+                                       uint16_t* scale_out, uint32_t* flags, cudaStream_t stream);
+
+}  // namespace coat

@@ -1,0 +1,173 @@
+"""GPU parity: the fused FP8-DRE AdamW step (K1) vs coatsim::step.
+
+Reference: optimizer.cpp:90-114 with the {E4M3, expand, 128} policy for both
+moments.  Bit-exact on the updated fp32 weights, codes, BF16 scales, k and c,
+over multi-step trajectories, ragged sizes and the error semantics.
+"""
+import numpy as np
+import pytest
+
+from conftest import rng
+
+pytestmark = pytest.mark.gpu
+
+CFG = {"beta1": 0.9, "beta2": 0.999, "lr": 1e-3, "weight_decay": 0.1, "eps": 1e-8}
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    import torch
+    return (t.float() if t.dtype == torch.bfloat16 else t).cpu().numpy()
+
+
+def gpu_state(slot):
+    out = []
+    for st in (slot.m, slot.v):
+        out.append({"codes": host(st.quantized.codes), "scales": host(st.quantized.scales),
+                    "k": host(st.k), "c": host(st.c)})
+    return out
+
+
+def assert_state_equal(got, exp, what=""):
+    for key in ("codes", "scales", "k", "c"):
+        a, b = got[key], exp[key]
+        bad = np.nonzero(a.view(np.uint8 if key == "codes" else np.uint32)
+                         != b.view(np.uint8 if key == "codes" else np.uint32))[0]
+        assert bad.size == 0, (what, key, bad[:8], a[bad[:8]], b[bad[:8]])
+
+
+def run_both(coat, port, n, steps, cfg=CFG, seed=1, warm=None, grad_scale=1e-3):
+    w0 = port.generate(0, (n,), 0.0, 100.0, seed) * np.float32(0.02)
+    w_ref = w0.copy()
+    m, v = port.make_slot(n)
+    slot = coat.make_slot([n])
+    if warm is not None:
+        m, v = warm
+        slot.load_state(m, v, 9)
+        m = {k: a.copy() for k, a in m.items()}
+        v = {k: a.copy() for k, a in v.items()}
+    t0 = slot.step
+    w = dev(w0)
+    c = coat.AdamWConfig(**cfg)
+    for t in range(steps):
+        g = port.generate(0, (n,), 0.01, 100.0, 100 + t) * np.float32(grad_scale)
+        assert port.step(w_ref, g, m, v, t0 + t, cfg) == 0
+        coat.step(w, dev(g), slot, c)
+        gm, gv = gpu_state(slot)
+        wd = host(w)
+        bad = np.nonzero(wd.view(np.uint32) != w_ref.view(np.uint32))[0]
+        assert bad.size == 0, (t, bad[:8], wd[bad[:8]], w_ref[bad[:8]])
+        assert_state_equal(gm, m, f"m step {t}")
+        assert_state_equal(gv, v, f"v step {t}")
+    assert slot.step == t0 + steps
+
+
+@pytest.mark.parametrize("n", [128, 512, 4096, 5000, 1000 * 128 + 3, 1 << 16])
+def test_step_trajectory_bit_exact(coat, port, n):
+    run_both(coat, port, n, 5)
+
+
+def test_step_from_warmed_state(coat, port):
+    """Fixture (B) of SURVEY.md 8(d): m with k ~ 1-3, v with k ~ 5-15, t = 10."""
+    groups = 2048
+    n = groups * 128
+    m0 = port.generate(0, (n,), 0.01, 100.0, 21) * np.float32(1e-4)
+    r = rng(22)
+    v0 = np.concatenate([np.exp(r.uniform(-0.5 * np.log(q), 0.5 * np.log(q), 128)) * 1e-8
+                         for q in r.uniform(2.5, 11.0, groups)]).astype(np.float32)
+    mc, ms, mk, mcc = port.expand_quantize(m0)
+    vc, vs, vk, vcc = port.expand_quantize(v0)
+    warm = ({"codes": mc, "scales": ms, "k": mk, "c": mcc}, {"codes": vc, "scales": vs, "k": vk, "c": vcc})
+    run_both(coat, port, n, 3, warm=warm)
+
+
+def test_step_without_weight_decay_and_large_grads(coat, port):
+    run_both(coat, port, 1 << 14, 3, cfg=dict(CFG, weight_decay=0.0), grad_scale=1.0)
+
+
+def test_step_kat_first_step(coat):
+    """t = 1, g = 1, zero state -> w - lr/(1+eps) per element (wd = 0)."""
+    import torch
+    n = 1024
+    slot = coat.make_slot([n])
+    w = torch.zeros(n, device="cuda")
+    coat.step(w, torch.ones(n, device="cuda"), slot, coat.AdamWConfig(lr=1e-3))
+    expect = np.float32(0) - np.float32(1e-3) * (np.float32(1) / (np.float32(1) + np.float32(1e-8)))
+    assert np.all(host(w) == expect)
+
+
+def test_nonfinite_grad_leaves_everything_untouched(coat):
+    import torch
+    n = 4096
+    slot = coat.make_slot([n])
+    w = torch.randn(n, device="cuda")
+    c = coat.AdamWConfig(weight_decay=0.1)
+    coat.step(w, torch.randn(n, device="cuda") * 1e-3, slot, c)
+    w_before = w.clone()
+    m_before = slot.m.quantized.codes.clone()
+    g = torch.randn(n, device="cuda")
+    g[1234] = float("nan")
+    with pytest.raises(coat.NonFiniteGradient):
+        coat.step(w, g, slot, c)
+    assert torch.equal(w, w_before) and torch.equal(slot.m.quantized.codes, m_before)
+    assert slot.step == 1
+
+
+def test_pack_failure_commits_like_reference(coat, port):
+    """g*g overflow -> v = inf -> pack_moment(v) throws: params and m committed,
+    v and the step counter not (optimizer.cpp:101-114)."""
+    import torch
+    n = 512
+    slot = coat.make_slot([n])
+    w = torch.ones(n, device="cuda")
+    g = torch.zeros(n, device="cuda")
+    g[3] = 1e20
+    v_before = slot.v.quantized.codes.clone()
+    with pytest.raises(coat.NonFiniteInput):
+        coat.step(w, g, slot, coat.AdamWConfig(weight_decay=0.1))
+    # reference
+    wr = np.ones(n, np.float32)
+    m, v = port.make_slot(n)
+    m0 = {k: a.copy() for k, a in m.items()}
+    assert port.step(wr, host(g), m, v, 0, dict(CFG)) == 3
+    assert np.array_equal(host(w), wr)
+    assert torch.equal(slot.v.quantized.codes, v_before)
+    assert np.array_equal(host(slot.m.quantized.codes), m["codes"])
+    assert slot.step == 0
+
+
+def test_shape_and_policy_errors(coat):
+    import torch
+    slot = coat.make_slot([256])
+    with pytest.raises(coat.ShapeMismatch):
+        coat.step(torch.zeros(255, device="cuda"), torch.zeros(255, device="cuda"), slot, coat.AdamWConfig())
+    with pytest.raises(coat.ShapeMismatch):
+        coat.step(torch.zeros(256, device="cuda"), torch.zeros(128, device="cuda"), slot, coat.AdamWConfig())
+    with pytest.raises(coat.InvalidSpec):
+        coat.make_slot([256], coat.SlotPolicy(coat.MomentPolicy(coat.StateFormat.DE8)))
+
+
+def test_step_16m_against_multithreaded_reference(coat, ref):
+    """Config 1 size (2^24 params), two steps from zero state + warmed state,
+    against the unmodified reference run on all host cores."""
+    import os
+    n = 1 << 24
+    th = os.cpu_count() or 8
+    w0 = ref.generate(0, (n,), 0.0, 100.0, 1) * np.float32(0.02)
+    w_ref = w0.copy()
+    m, v = ref.make_slot(n)
+    slot = coat.make_slot([n])
+    w = dev(w0)
+    c = coat.AdamWConfig(**CFG)
+    for t in range(2):
+        g = ref.generate(0, (n,), 0.01, 100.0, 100 + t) * np.float32(1e-3)
+        assert ref.step(w_ref, g, m, v, t, CFG, threads=th) == 0
+        coat.step(w, dev(g), slot, c)
+    gm, gv = gpu_state(slot)
+    assert np.array_equal(host(w).view(np.uint32), w_ref.view(np.uint32))
+    assert_state_equal(gm, m, "m")
+    assert_state_equal(gv, v, "v")
