@@ -133,6 +133,17 @@ coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g,
                                 coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t,
                                 uint32_t* d_flags, void* stream);
 
+/* The same step with HOST-resident params/grads (the reference's Tensor lives
+ * in host memory) and the state resident in HBM: w/g are streamed through the
+ * GPU in `chunk`-parameter pieces on three CUDA streams (H2D, K1, D2H
+ * overlapped).  w_host_in/g_host/w_host_out should be pinned host memory;
+ * w_host_out may alias w_host_in.  chunk <= 0 selects 32 Mi parameters. */
+coat_status coat_adamw_dre_step_host(const float* w_host_in, float* w_host_out, const float* g_host,
+                                     int64_t n, int64_t group_size, coat_moment_state m_in,
+                                     coat_moment_state v_in, coat_moment_state m_out,
+                                     coat_moment_state v_out, const coat_adamw_config* cfg,
+                                     int64_t t, uint32_t* d_flags, int64_t chunk, void* stream);
+
 /* Test/diagnostic hook: count elements that took the literal (double pow)
  * fallback in DRE kernels into *d_counter (device u64); NULL disables. */
 coat_status coat_set_fallback_counter(unsigned long long* d_counter);

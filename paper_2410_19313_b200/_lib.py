@@ -66,6 +66,9 @@ _SIGS = {
     "coat_make_slot": ([_i64, _i64, MomentState, MomentState, _vp], _int),
     "coat_adamw_dre_step": ([_vp, _vp, _vp, _i64, _i64, MomentState, MomentState, MomentState,
                              MomentState, C.POINTER(AdamWConfigC), _i64, _vp, _vp], _int),
+    "coat_adamw_dre_step_host": ([_vp, _vp, _vp, _i64, _i64, MomentState, MomentState,
+                                  MomentState, MomentState, C.POINTER(AdamWConfigC), _i64, _vp,
+                                  _i64, _vp], _int),
     "coat_set_fallback_counter": ([_vp], _int),
 }
 

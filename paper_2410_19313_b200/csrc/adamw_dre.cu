@@ -394,10 +394,26 @@ cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* 
     S.bc1 = a.bc1;
     S.bc2 = a.bc2;
     S.log_target = a.log_target;
-    const int64_t ng = (n + dre::kG - 1) / dre::kG;
+    // Full 512-parameter tiles go through the TMA-pipelined kernel (k1_fast.cu);
+    // the ragged tail (and misaligned buffers) through the generic kernel below.
+    int64_t done = 0;
+    if (!fallbacks) {
+        const int64_t nfull = n / kTile;
+        const cudaError_t e = launch_k1_fast(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream);
+        if (e == cudaSuccess) done = nfull * kTile;
+        else if (e != cudaErrorNotSupported) return e;
+    }
+    if (done == n) return cudaSuccess;
+    const int64_t gdone = done / dre::kG;
+    const MomentStateIn mi{m_in.codes + done, m_in.scales + gdone, m_in.k + gdone, m_in.c + gdone};
+    const MomentStateIn vi{v_in.codes + done, v_in.scales + gdone, v_in.k + gdone, v_in.c + gdone};
+    const MomentStateOut mo{m_out.codes + done, m_out.scales + gdone, m_out.k + gdone, m_out.c + gdone};
+    const MomentStateOut vo{v_out.codes + done, v_out.scales + gdone, v_out.k + gdone, v_out.c + gdone};
+    const int64_t rest = n - done;
+    const int64_t ng = (rest + dre::kG - 1) / dre::kG;
     const int64_t ntiles = (ng + kTileGroups - 1) / kTileGroups;
     adamw_dre_step_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(
-        w_in, w_out, g, n, m_in, v_in, m_out, v_out, S, flags, fallbacks);
+        w_in + done, w_out + done, g + done, rest, mi, vi, mo, vo, S, flags, fallbacks);
     return cudaGetLastError();
 }
 
@@ -405,8 +421,19 @@ cudaError_t launch_expand_quantize(const float* x, int64_t n, const MomentStateO
                                    double log_target, uint32_t* flags,
                                    unsigned long long* fallbacks, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
-    const int64_t ntiles = (n / dre::kG + kTileGroups - 1) / kTileGroups;
-    expand_quantize_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(x, n, out, log_target,
+    int64_t done = 0;
+    if (!fallbacks && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out.codes)) & 15u) == 0) {
+        const int64_t nfull = n / kTile;
+        const cudaError_t e = launch_expand_quantize_fast(x, nfull, out, log_target, flags, stream);
+        if (e != cudaSuccess) return e;
+        done = nfull * kTile;
+    }
+    if (done == n) return cudaSuccess;
+    const int64_t gd = done / dre::kG;
+    const MomentStateOut o{out.codes + done, out.scales + gd, out.k + gd, out.c + gd};
+    const int64_t rest = n - done;
+    const int64_t ntiles = (rest / dre::kG + kTileGroups - 1) / kTileGroups;
+    expand_quantize_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(x + done, rest, o, log_target,
                                                                                flags, fallbacks);
     return cudaGetLastError();
 }
@@ -414,8 +441,19 @@ cudaError_t launch_expand_quantize(const float* x, int64_t n, const MomentStateO
 cudaError_t launch_dequantize_contract(const MomentStateIn& in, int64_t n, float* x, uint32_t* flags,
                                        cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
-    const int64_t ntiles = (n / dre::kG + kTileGroups - 1) / kTileGroups;
-    dequantize_contract_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(in, n, x, flags);
+    int64_t done = 0;
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(in.codes)) & 15u) == 0) {
+        const int64_t nfull = n / kTile;
+        const cudaError_t e = launch_dequantize_contract_fast(in, nfull, x, flags, stream);
+        if (e != cudaSuccess) return e;
+        done = nfull * kTile;
+    }
+    if (done == n) return cudaSuccess;
+    const int64_t gd = done / dre::kG;
+    const MomentStateIn i2{in.codes + done, in.scales + gd, in.k + gd, in.c + gd};
+    const int64_t rest = n - done;
+    const int64_t ntiles = (rest / dre::kG + kTileGroups - 1) / kTileGroups;
+    dequantize_contract_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(i2, rest, x + done, flags);
     return cudaGetLastError();
 }
 

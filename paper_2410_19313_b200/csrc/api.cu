@@ -178,18 +178,15 @@ coat_status coat_make_slot(int64_t n, int64_t G, coat_moment_state m, coat_momen
     return cuda_status(e);
 }
 
-coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n, int64_t G,
-                                coat_moment_state m_in, coat_moment_state v_in, coat_moment_state m_out,
-                                coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t,
-                                uint32_t* d_flags, void* stream) {
+static coat_status step_args(const coat_adamw_config* cfg, int64_t n, int64_t G, int64_t t,
+                             const coat_moment_state& m_in, const coat_moment_state& v_in,
+                             const coat_moment_state& m_out, const coat_moment_state& v_out, AdamWScalars& a) {
     if (!cfg) return fail(COAT_ERR_INVALID, "step: cfg is NULL");
     if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
     if (G != 128) return fail(COAT_ERR_INVALID, "step: only G = 128 is implemented on B200");
     if (t < 1) return fail(COAT_ERR_INVALID, "step: t is the 1-based step number");
-    if (!w_in || !w_out || !g) return fail(COAT_ERR_INVALID, "step: NULL buffer");
     if (!state_ok(m_in) || !state_ok(v_in) || !state_ok(m_out) || !state_ok(v_out))
         return fail(COAT_ERR_INVALID, "step: misaligned or NULL state buffer");
-    AdamWScalars a;
     a.beta1 = cfg->beta1;
     a.beta2 = cfg->beta2;
     a.lr = cfg->lr;
@@ -199,6 +196,31 @@ coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g,
     a.bc1 = 1.0f - std::pow(cfg->beta1, float(t));
     a.bc2 = 1.0f - std::pow(cfg->beta2, float(t));
     a.log_target = kLogTarget;
+    return COAT_OK;
+}
+
+coat_status coat_adamw_dre_step_host(const float* w_host_in, float* w_host_out, const float* g_host, int64_t n,
+                                     int64_t G, coat_moment_state m_in, coat_moment_state v_in,
+                                     coat_moment_state m_out, coat_moment_state v_out,
+                                     const coat_adamw_config* cfg, int64_t t, uint32_t* d_flags, int64_t chunk,
+                                     void* stream) {
+    AdamWScalars a;
+    const coat_status st = step_args(cfg, n, G, t, m_in, v_in, m_out, v_out, a);
+    if (st != COAT_OK) return st;
+    if (!w_host_in || !w_host_out || !g_host) return fail(COAT_ERR_INVALID, "step: NULL buffer");
+    if (chunk <= 0) chunk = int64_t(32) << 20;
+    return cuda_status(host_pipelined_step(w_host_in, w_host_out, g_host, n, m_in, v_in, m_out, v_out, a,
+                                           d_flags, g_fallback_counter, chunk, S(stream)));
+}
+
+coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n, int64_t G,
+                                coat_moment_state m_in, coat_moment_state v_in, coat_moment_state m_out,
+                                coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t,
+                                uint32_t* d_flags, void* stream) {
+    AdamWScalars a;
+    const coat_status st = step_args(cfg, n, G, t, m_in, v_in, m_out, v_out, a);
+    if (st != COAT_OK) return st;
+    if (!w_in || !w_out || !g) return fail(COAT_ERR_INVALID, "step: NULL buffer");
     return cuda_status(launch_adamw_dre_step(w_in, w_out, g, n, in_of(m_in), in_of(v_in), out_of(m_out),
                                              out_of(v_out), a, d_flags, g_fallback_counter, S(stream)));
 }

@@ -34,12 +34,30 @@ cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* 
                                   const MomentStateOut& m_out, const MomentStateOut& v_out,
                                   const AdamWScalars& a, uint32_t* flags,
                                   unsigned long long* fallbacks, cudaStream_t stream);
+cudaError_t launch_k1_fast(const float* w_in, float* w_out, const float* g, int64_t ntiles,
+                           const MomentStateIn& m_in, const MomentStateIn& v_in, const MomentStateOut& m_out,
+                           const MomentStateOut& v_out, const AdamWScalars& a, uint32_t* flags,
+                           cudaStream_t stream);
+cudaError_t launch_expand_quantize_fast(const float* x, int64_t ntiles, const MomentStateOut& out,
+                                        double log_target, uint32_t* flags, cudaStream_t stream);
+cudaError_t launch_dequantize_contract_fast(const MomentStateIn& in, int64_t ntiles, float* x, uint32_t* flags,
+                                            cudaStream_t stream);
 cudaError_t launch_expand_quantize(const float* x, int64_t n, const MomentStateOut& out,
                                    double log_target, uint32_t* flags,
                                    unsigned long long* fallbacks, cudaStream_t stream);
 cudaError_t launch_dequantize_contract(const MomentStateIn& in, int64_t n, float* x,
                                        uint32_t* flags, cudaStream_t stream);
 cudaError_t launch_make_slot(const MomentStateOut& st, int64_t npad, cudaStream_t stream);
+
+// host_pipeline.cu: host-resident w/g streamed through K1 (state in HBM)
+}  // namespace coat
+#include "../../include/coat.h"
+namespace coat {
+cudaError_t host_pipelined_step(const float* w_host_in, float* w_host_out, const float* g_host, int64_t n,
+                                const coat_moment_state& m_in, const coat_moment_state& v_in,
+                                const coat_moment_state& m_out, const coat_moment_state& v_out,
+                                const AdamWScalars& a, uint32_t* flags, unsigned long long* fallbacks,
+                                int64_t chunk, cudaStream_t stream);
 
 // activation quantizers (act_quant.cu)
 cudaError_t launch_encode_e4m3(const float* x, uint8_t* out, int64_t n, uint32_t* flags,

@@ -84,7 +84,7 @@ __device__ __forceinline__ ContractParams contract_prepare(float s, float k, flo
 
 // Literal contract_one (expand.cpp:24-28) on y = decode(code)*s (fp32 product,
 // quantize.cpp:122).
-__device__ __noinline__ float contract_literal(uint32_t code, float s, float k, float c) {
+static __device__ __noinline__ float contract_literal(uint32_t code, float s, float k, float c) {
     const float y = __fmul_rn(e4m3_decode(code), s);
     if (y == 0.0f) return 0.0f;
     const double mag = pow(fabs((double)y), 1.0 / (double)k) * (double)c;
@@ -178,7 +178,7 @@ __device__ __forceinline__ PackParams pack_prepare(float lo, float hi, double lo
 
 // Literal expand_one + encode_scaled for one element (expand.cpp:18-22,
 // quantize.cpp:19-27).
-__device__ __noinline__ uint32_t pack_literal(float x, float k, float c, float s) {
+static __device__ __noinline__ uint32_t pack_literal(float x, float k, float c, float s) {
     if (x == 0.0f) return 0u;
     const double ratio = fabs((double)x) / (double)c;
     const double mag = k == 1.0f ? ratio : pow(ratio, (double)k);
