@@ -188,12 +188,12 @@ static __device__ __noinline__ uint32_t pack_literal(float x, float k, float c, 
 
 __device__ __forceinline__ float lg2_approx(float x) {
     float r;
-    asm("lg2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 __device__ __forceinline__ float ex2_approx(float x) {
     float r;
-    asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 

@@ -200,22 +200,32 @@ static __device__ __noinline__ PackParams pack_prepare_fast(uint32_t lo_bits, ui
 }
 
 // Codes of 4 values of one group; bit i of `unsure` marks an element that
-// needs the literal formula.  x must not be -0 (callers canonicalize).
+// needs the literal formula.  x must not be -0 (callers canonicalize).  The
+// lg2/ex2 inputs are never subnormal here (r in [2^-9, 2^9] for k > 1), so
+// the .ftz SFU forms are exact replacements of the non-ftz ones.
 __device__ __forceinline__ uint32_t pack_word(const float (&x)[4], const PackParams& p, uint32_t& unsure) {
     float qlo[4], qhi[4];
-    const float rlo = 1.0f - (p.mode == 0 ? kRelLinear : kRelMufu);
-    const float rhi = 1.0f + (p.mode == 0 ? kRelLinear : kRelMufu);
+    if (p.mode == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float r = __fmul_rn(fabsf(x[i]), p.inv_c);
-        const float e = p.mode == 0 ? r : ex2_approx(__fmul_rn(p.k, lg2_approx(r)));
-        const float q = u2f(f2u(__fmul_rn(e, p.inv_s)) | (f2u(x[i]) & 0x80000000u));
-        qlo[i] = __fmul_rn(q, rlo);
-        qhi[i] = __fmul_rn(q, rhi);
+        for (int i = 0; i < 4; ++i) {
+            const float e = __fmul_rn(fabsf(x[i]), p.inv_c);
+            const float q = u2f(f2u(__fmul_rn(e, p.inv_s)) | (f2u(x[i]) & 0x80000000u));
+            qlo[i] = __fmul_rn(q, 1.0f - kRelLinear);
+            qhi[i] = __fmul_rn(q, 1.0f + kRelLinear);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float e = ex2_approx(__fmul_rn(p.k, lg2_approx(__fmul_rn(fabsf(x[i]), p.inv_c))));
+            const float q = u2f(f2u(__fmul_rn(e, p.inv_s)) | (f2u(x[i]) & 0x80000000u));
+            qlo[i] = __fmul_rn(q, 1.0f - kRelMufu);
+            qhi[i] = __fmul_rn(q, 1.0f + kRelMufu);
+        }
     }
     const uint32_t lo01 = cvt_e4m3x2(qlo[0], qlo[1]), hi01 = cvt_e4m3x2(qhi[0], qhi[1]);
     const uint32_t lo23 = cvt_e4m3x2(qlo[2], qlo[3]), hi23 = cvt_e4m3x2(qhi[2], qhi[3]);
-    unsure |= (lo01 != hi01 ? 0x3u : 0u) | (lo23 != hi23 ? 0xCu : 0u) | (p.mode == 2 ? 0xFu : 0u);
+    unsure |= (lo01 != hi01 ? 0x3u : 0u) | (lo23 != hi23 ? 0xCu : 0u);
+    if (p.mode == 2) unsure = 0xFu;
     return lo01 | (lo23 << 16);
 }
 
