@@ -203,30 +203,31 @@ static __device__ __noinline__ PackParams pack_prepare_fast(uint32_t lo_bits, ui
 // needs the literal formula.  x must not be -0 (callers canonicalize).  The
 // lg2/ex2 inputs are never subnormal here (r in [2^-9, 2^9] for k > 1), so
 // the .ftz SFU forms are exact replacements of the non-ftz ones.
-__device__ __forceinline__ uint32_t pack_word(const float (&x)[4], const PackParams& p, uint32_t& unsure) {
-    float qlo[4], qhi[4];
-    if (p.mode == 0) {
+__device__ __forceinline__ uint32_t pack_word(const float (&x)[4], const PackParams& p, uint32_t& unsure, float nz) {
+    F2 q[2];
+    const float rel = p.mode == 0 ? kRelLinear : kRelMufu;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float e = __fmul_rn(fabsf(x[i]), p.inv_c);
-            const float q = u2f(f2u(__fmul_rn(e, p.inv_s)) | (f2u(x[i]) & 0x80000000u));
-            qlo[i] = __fmul_rn(q, 1.0f - kRelLinear);
-            qhi[i] = __fmul_rn(q, 1.0f + kRelLinear);
+    for (int h = 0; h < 2; ++h) {
+        const F2 ax{fabsf(x[2 * h]), fabsf(x[2 * h + 1])};
+        const F2 r = f2_mul(ax, f2s(p.inv_c), nz);
+        F2 e;
+        if (p.mode == 0) {
+            e = r;
+        } else {
+            const F2 l{lg2_approx(r.x), lg2_approx(r.y)};
+            const F2 u = f2_mul(l, f2s(p.k), nz);
+            e = F2{ex2_approx(u.x), ex2_approx(u.y)};
         }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float e = ex2_approx(__fmul_rn(p.k, lg2_approx(__fmul_rn(fabsf(x[i]), p.inv_c))));
-            const float q = u2f(f2u(__fmul_rn(e, p.inv_s)) | (f2u(x[i]) & 0x80000000u));
-            qlo[i] = __fmul_rn(q, 1.0f - kRelMufu);
-            qhi[i] = __fmul_rn(q, 1.0f + kRelMufu);
-        }
+        const F2 qq = f2_mul(e, f2s(p.inv_s), nz);
+        q[h] = F2{u2f(f2u(qq.x) | (f2u(x[2 * h]) & 0x80000000u)), u2f(f2u(qq.y) | (f2u(x[2 * h + 1]) & 0x80000000u))};
     }
-    const uint32_t lo01 = cvt_e4m3x2(qlo[0], qlo[1]), hi01 = cvt_e4m3x2(qhi[0], qhi[1]);
-    const uint32_t lo23 = cvt_e4m3x2(qlo[2], qlo[3]), hi23 = cvt_e4m3x2(qhi[2], qhi[3]);
-    unsure |= (lo01 != hi01 ? 0x3u : 0u) | (lo23 != hi23 ? 0xCu : 0u);
+    const F2 lo01 = f2_mul(q[0], f2s(1.0f - rel), nz), hi01 = f2_mul(q[0], f2s(1.0f + rel), nz);
+    const F2 lo23 = f2_mul(q[1], f2s(1.0f - rel), nz), hi23 = f2_mul(q[1], f2s(1.0f + rel), nz);
+    const uint32_t c01 = cvt_e4m3x2(lo01.x, lo01.y), d01 = cvt_e4m3x2(hi01.x, hi01.y);
+    const uint32_t c23 = cvt_e4m3x2(lo23.x, lo23.y), d23 = cvt_e4m3x2(hi23.x, hi23.y);
+    unsure |= (c01 != d01 ? 0x3u : 0u) | (c23 != d23 ? 0xCu : 0u);
     if (p.mode == 2) unsure = 0xFu;
-    return lo01 | (lo23 << 16);
+    return c01 | (c23 << 16);
 }
 
 __device__ __forceinline__ void fix_contract(float (&x)[4], uint32_t unsure, uint32_t codes, const PairContract& P) {
