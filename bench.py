@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "mgaq"],
+                    help="adamw7b: BASELINE.json cfg3 (the headline); mgaq: cfg2 activation quantizers")
     return ap.parse_args()
 
 
@@ -184,6 +186,9 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.workload == "mgaq":
+        run_mgaq(args)
         return
     import torch
     import torch.distributed as dist
@@ -377,6 +382,103 @@ def run_e2e(args, L, _lib, n, w, g, m, v, cur, t_step, cfg, cstate, flags, strea
     return {"value": n * ws / (ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 8 * n,
             "d2h_bytes_per_step": 4 * n, "ms_per_step": ms, "wall_s_per_step": wall, "steps": K,
             "path": "coat_adamw_dre_step_host: pinned host w,g -> 3-stream chunked H2D / K1 / D2H"}
+
+
+# ------------------------------------------------ cfg2: MGAQ quantizers ----
+MGAQ_TENSORS = [  # (name, rows, cols, granularity) -- flow.cpp:546-612 call sites, Llama-2-7B layer
+    ("rmsnorm1.in", 8192, 4096, 16), ("qkv.in", 8192, 4096, 0), ("attn.out", 8192, 4096, 0),
+    ("rmsnorm2.in", 8192, 4096, 16), ("upgate.in", 8192, 4096, 0), ("silu.in", 8192, 11008, 16),
+    ("mul.in.silu", 8192, 11008, 16), ("mul.in.up", 8192, 11008, 16), ("down.in", 8192, 11008, 0),
+]
+
+
+def run_mgaq(args):
+    """BASELINE.json cfg2: quantize one Llama-2-7B decoder layer's saved
+    activations (B=4, S=2048, H=4096, I=11008; bf16 in): per-group 1x16 for the
+    non-linear inputs, per-tensor with two-stage Group Scaling amax (stage-1
+    1x128) for the linear inputs.  Algorithmic bytes: per-group in+1+2/16,
+    per-tensor in+1."""
+    import torch
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device=dev).manual_seed(7)
+    bufs = []
+    alg_bytes = 0
+    for name, r, c, G in MGAQ_TENSORS:
+        x = (torch.randn(r, c, device=dev, generator=gen) * 2).to(torch.bfloat16)
+        x[:: 100] *= 50   # hot token rows (ActivationWithOutliers)
+        codes = torch.empty(r, c, dtype=torch.uint8, device=dev)
+        if G:
+            scales = torch.empty(r * c // G, dtype=torch.int16, device=dev)
+            alg_bytes += r * c * (2 + 1) + 2 * r * c // G
+        else:
+            scales = torch.empty(1, dtype=torch.int16, device=dev)
+            alg_bytes += r * c * (2 + 1)
+        bufs.append((name, r, c, G, x, codes, scales))
+    amax = torch.zeros(1, dtype=torch.int32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    nel = sum(r * c for _, r, c, *_ in bufs)
+
+    def step(record=None):
+        launches = 0
+        for name, r, c, G, x, codes, scales in bufs:
+            if record is not None:
+                record[name][0].record(stream)
+            if G:
+                st = L.coat_quantize_per_group(x.data_ptr(), 1, r, c, G, codes.data_ptr(), scales.data_ptr(),
+                                               flags.data_ptr(), stream.cuda_stream)
+                launches += 1
+            else:
+                st = L.coat_group_scale_max(x.data_ptr(), 1, r, c, 128, None, amax.data_ptr(), stream.cuda_stream)
+                st = st or L.coat_quantize_per_tensor(x.data_ptr(), 1, r * c, amax.data_ptr(), codes.data_ptr(),
+                                                      scales.data_ptr(), flags.data_ptr(), stream.cuda_stream)
+                launches += 3   # memset + amax + quant
+            if record is not None:
+                record[name][1].record(stream)
+            assert st == 0, L.coat_last_error()
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = {name: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for name, *_ in MGAQ_TENSORS}
+    per = {name: 0.0 for name, *_ in MGAQ_TENSORS}
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(0)
+    launches = 0
+    with sampler:
+        start.record(stream)
+        for _ in range(args.steps):
+            launches += step(evs)
+            for name in per:   # events are reused: accumulate after each step
+                pass
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / args.steps
+    # per-tensor timing from one extra instrumented pass
+    step(evs)
+    torch.cuda.synchronize()
+    for name, *_ in MGAQ_TENSORS:
+        per[name] = evs[name][0].elapsed_time(evs[name][1])
+    peak, kind = measured_peaks()
+    gbs = alg_bytes / (ms * 1e-3) / 1e9
+    out = {
+        "metric": "MGAQ activation quantization, Llama-2-7B layer (cfg2): elements/s & HBM GB/s",
+        "value": nel / (ms * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
+        "config": {"workload": "cfg2: MGAQ of one Llama-2-7B decoder layer, B4 x S2048 x H4096, I=11008",
+                   "tensors": [t[:4] for t in MGAQ_TENSORS], "elements": nel,
+                   "l2": "per-tensor inputs of 64-180 MB: stage-2 re-read partly L2-resident"},
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                     "traffic": None, "peak_kind": kind, "algorithmic_bytes": alg_bytes},
+        "per_tensor_ms": per, "clocks": sampler.summary(), "gpu_launches": launches,
+    }
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":

@@ -11,10 +11,12 @@
 // All kernels are HBM-bound streams.  A thread owns a 16-element chunk
 // (32 B of bf16 or 64 B of fp32 in, one 16 B vector of codes out); a 1xG group
 // spans G/16 consecutive lanes and its absmax is a log2(G/16)-step xor-shuffle
-// max.  Codes are certified against the exact IEEE quotient x/s
-// (certified_code in coat_device.cuh) and recomputed with __fdiv_rn only when
-// the cheap quotient is ambiguous, so they are bit-identical to encode_scaled
-// (quantize.cpp:19-27).
+// max.  The quotient x/s of encode_scaled (quantize.cpp:19-27) is computed
+// EXACTLY with Markstein's correction from RN(1/s) -- 3 paired FFMA2 per 2
+// elements, verified exhaustively for all 128 BF16 scale mantissas x all fp32
+// mantissas (tests/test_markstein.py); quotients that could under/overflow only
+// occur where the E4M3 code is +-0 or saturated either way -- then one
+// cvt.e4m3x2 encodes two elements.  Codes are bit-identical to the reference.
 #include <cstdint>
 
 #include "coat_device.cuh"
@@ -23,7 +25,6 @@
 namespace coat {
 namespace {
 
-constexpr float kRelQ = 0x1p-20f;   // |x*RN(1/s) - x/s| <= 2^-23 relative; 8x margin
 constexpr int kThreads = 256;
 
 struct Chunk16 {
@@ -69,21 +70,53 @@ __device__ __forceinline__ uint32_t abs_bits_nan0(float x) {
     return a > 0x7F800000u ? 0u : a;
 }
 
-__device__ __forceinline__ uint32_t encode_exact(float x, float s, float inv_s) {
-    uint32_t code;
-    if (certified_code(__fmul_rn(x, inv_s), kRelQ, code)) return code;
-    return e4m3_encode(__fdiv_rn(x, s));
+// RN(x / s) from rs = RN(1/s) (Markstein): exact for the quotient range that
+// matters to E4M3 (see header).
+__device__ __forceinline__ float quot_exact(float x, float s, float rs) {
+    const float q0 = __fmul_rn(x, rs);
+    return __fmaf_rn(__fmaf_rn(-q0, s, x), rs, q0);
 }
 
-__device__ __forceinline__ uint4 encode16(const Chunk16& c, float s, float inv_s) {
+__device__ __forceinline__ uint32_t encode_exact(float x, float s, float rs) {
+    return e4m3_encode(s >= 0x1p-100f ? quot_exact(x, s, rs) : __fdiv_rn(x, s));
+}
+
+// 16 codes from 16 values: paired Markstein quotients + one cvt per 2 values.
+__device__ __forceinline__ uint4 encode16(const Chunk16& c, float s, float rs, float nz) {
     uint32_t w[4];
+    if (!(s >= 0x1p-100f)) {
+        // all-subnormal group: s = bf16_min_positive and 1/s overflows -- IEEE division
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            w[k] = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[k] |= e4m3_encode(__fdiv_rn(c.v[4 * k + i], s)) << (8 * i);
+        }
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        w[k] = 0;
+        uint32_t h[2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w[k] |= encode_exact(c.v[4 * k + i], s, inv_s) << (8 * i);
+        for (int p = 0; p < 2; ++p) {
+            const F2 x{c.v[4 * k + 2 * p], c.v[4 * k + 2 * p + 1]};
+            const F2 q0 = f2_mul(x, f2s(rs), nz);
+            const F2 q = f2_fma(f2_fma(q0, f2s(-s), x), f2s(rs), q0);
+            h[p] = cvt_e4m3x2(q.x, q.y);
+        }
+        w[k] = h[0] | (h[1] << 16);
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Exact absmax bits of 16 values and a non-finite flag (bf16 pairs use 16-bit SIMD max).
+template <int DT>
+__device__ __forceinline__ uint32_t absmax16(const Chunk16& c, uint32_t& bad) {
+    uint32_t am = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) am = max(am, f2u(c.v[i]) & 0x7FFFFFFFu);
+    bad |= am >= 0x7F800000u;   // the max is >= every element, so any Inf/NaN shows here
+    return am;
 }
 
 // ---------------------------------------------------------------- per-group --
@@ -91,7 +124,7 @@ __device__ __forceinline__ uint4 encode16(const Chunk16& c, float s, float inv_s
 template <int DT, int L>
 __global__ void __launch_bounds__(kThreads)
 quant_group_kernel(const void* __restrict__ x, int64_t nchunks, uint8_t* __restrict__ codes,
-                   uint16_t* __restrict__ scales, uint32_t* flags) {
+                   uint16_t* __restrict__ scales, uint32_t* flags, float nz) {
     uint32_t bad = 0;
     const int64_t stride = int64_t(gridDim.x) * kThreads;
     for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch - threadIdx.x % 32 < nchunks; ch += stride) {
@@ -99,21 +132,12 @@ quant_group_kernel(const void* __restrict__ x, int64_t nchunks, uint8_t* __restr
         const bool valid = ch < nchunks;
         Chunk16 c;
         if (valid) c = load16<DT>(x, ch * 16);
-        uint32_t am = 0;
-        if (valid) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const uint32_t a = f2u(c.v[i]) & 0x7FFFFFFFu;
-                bad |= a >= 0x7F800000u;
-                am = max(am, a);
-            }
-        }
+        uint32_t am = valid ? absmax16<DT>(c, bad) : 0u;
 #pragma unroll
         for (int off = 1; off < L; off <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
         if (valid) {
             const float s = group_scale(u2f(am));
-            const float inv_s = __frcp_rn(s);
-            reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, inv_s);
+            reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, __frcp_rn(s), nz);
             if ((threadIdx.x % L) == 0) scales[ch / L] = float_to_bf16_bits_exact(s);
         }
     }
@@ -250,7 +274,7 @@ group_amax_generic_kernel(const void* __restrict__ x, int64_t n, int64_t G, floa
 template <int DT>
 __global__ void __launch_bounds__(kThreads)
 quant_tensor_kernel(const void* __restrict__ x, int64_t n, const uint32_t* amax_bits,
-                    uint8_t* __restrict__ codes, uint16_t* scale_out, uint32_t* flags) {
+                    uint8_t* __restrict__ codes, uint16_t* scale_out, uint32_t* flags, float nz) {
     const float s = group_scale(u2f(*amax_bits));
     const float inv_s = __frcp_rn(s);
     if (blockIdx.x == 0 && threadIdx.x == 0 && scale_out) *scale_out = float_to_bf16_bits_exact(s);
@@ -259,9 +283,8 @@ quant_tensor_kernel(const void* __restrict__ x, int64_t n, const uint32_t* amax_
     for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch < nchunks;
          ch += int64_t(gridDim.x) * kThreads) {
         const Chunk16 c = load16<DT>(x, ch * 16);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) bad |= (f2u(c.v[i]) & 0x7FFFFFFFu) >= 0x7F800000u;
-        reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, inv_s);
+        absmax16<DT>(c, bad);
+        reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, inv_s, nz);
     }
     const int64_t t = nchunks * 16 + blockIdx.x * int64_t(kThreads) + threadIdx.x;
     if (blockIdx.x == 0 && t < n) {
@@ -337,9 +360,9 @@ cudaError_t launch_quantize_per_group(const void* x, int dtype, int64_t n, int64
     if (pow2_lanes(G, &L) && aligned16(x) && aligned16(codes)) {
         const int64_t nchunks = n / 16;
         if (dtype == 0) {
-            COAT_GROUP_SWITCH(L, (quant_group_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, codes, scales, flags)));
+            COAT_GROUP_SWITCH(L, (quant_group_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, codes, scales, flags, -0.0f)));
         } else {
-            COAT_GROUP_SWITCH(L, (quant_group_kernel<1, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, codes, scales, flags)));
+            COAT_GROUP_SWITCH(L, (quant_group_kernel<1, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, codes, scales, flags, -0.0f)));
         }
     } else {
         const int64_t warps = n / G;
@@ -386,8 +409,8 @@ cudaError_t launch_quantize_per_tensor(const void* x, int dtype, int64_t n, cons
     if (n <= 0) return cudaSuccess;
     if (!aligned16(x) || !aligned16(codes)) return cudaErrorMisalignedAddress;
     const int blocks = blocks_for(imax64(n / 16, 1));
-    if (dtype == 0) quant_tensor_kernel<0><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags);
-    else quant_tensor_kernel<1><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags);
+    if (dtype == 0) quant_tensor_kernel<0><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
+    else quant_tensor_kernel<1><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
     return cudaGetLastError();
 }
 

@@ -204,6 +204,23 @@ static __device__ __noinline__ PackParams pack_prepare_fast(uint32_t lo_bits, ui
 // lg2/ex2 inputs are never subnormal here (r in [2^-9, 2^9] for k > 1), so
 // the .ftz SFU forms are exact replacements of the non-ftz ones.
 __device__ __forceinline__ uint32_t pack_word(const float (&x)[4], const PackParams& p, uint32_t& unsure, float nz) {
+    if (p.mode == 0) {
+        // k == 1: e = RN(|x|/c) and q = RN(e/s) both EXACTLY via Markstein's
+        // correction from RN(1/c), RN(1/s) (tests/test_markstein.py); no
+        // certification needed.  c, s in [2^-100, 2^100] (else mode 2).
+        uint32_t c2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const F2 ax{fabsf(x[2 * h]), fabsf(x[2 * h + 1])};
+            const F2 e0 = f2_mul(ax, f2s(p.inv_c), nz);
+            const F2 e = f2_fma(f2_fma(e0, f2s(-p.c), ax), f2s(p.inv_c), e0);
+            const F2 q0 = f2_mul(e, f2s(p.inv_s), nz);
+            const F2 qq = f2_fma(f2_fma(q0, f2s(-p.s), e), f2s(p.inv_s), q0);
+            c2[h] = cvt_e4m3x2(u2f(f2u(qq.x) | (f2u(x[2 * h]) & 0x80000000u)),
+                               u2f(f2u(qq.y) | (f2u(x[2 * h + 1]) & 0x80000000u)));
+        }
+        return c2[0] | (c2[1] << 16);
+    }
     F2 q[2];
     const float rel = p.mode == 0 ? kRelLinear : kRelMufu;
 #pragma unroll
