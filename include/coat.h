@@ -1,7 +1,7 @@
 /* include/coat.h -- the drop-in C-ABI of the B200-native COAT hot path.
  *
  * Every entry point replaces one operator of the reference's proj/core API
- * (coatsim, /root/reference/proj/core/include/coatsim/*.hpp); the comment on
+ * (coatsim, /root/reference/proj/core/include/coatsim/), the comment on
  * each cites the reference declaration (file:line) it stands in for.  The
  * reference is a C++ library with no FFI of its own, so this header is the
  * boundary a binding (ctypes, the C++ shim in include/coat/coatsim_compat.hpp,
