@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
-    ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "mgaq"],
+    ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "mgaq", "linear"],
                     help="adamw7b: BASELINE.json cfg3 (the headline); mgaq: cfg2 activation quantizers")
     return ap.parse_args()
 
@@ -189,6 +189,9 @@ def main():
         return
     if args.workload == "mgaq":
         run_mgaq(args)
+        return
+    if args.workload == "linear":
+        run_linear(args)
         return
     import torch
     import torch.distributed as dist
@@ -477,6 +480,100 @@ def run_mgaq(args):
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "traffic": None, "peak_kind": kind, "algorithmic_bytes": alg_bytes},
         "per_tensor_ms": per, "clocks": sampler.summary(), "gpu_launches": launches,
+    }
+    print(json.dumps(out))
+
+
+# ----------------------------------------------- cfg4: FP8 linear fwd+bwd ----
+def run_linear(args):
+    """BASELINE.json cfg4: per-tensor FP8 E4M3 linear forward + backward with
+    Group Scaling amax, Llama-2-13B MLP shape (8192 tokens x 5120 x 13824).
+    One step = Group-Scaling quantize of x (bf16) and W (fp32), fwd GEMM
+    (E4M3 x E4M3, kind::f8f6f4), dgrad (BF16, kind::f16), wgrad (BF16)."""
+    import torch
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream()
+    M, K, N = 8192, 5120, 13824
+    g = torch.Generator(device=dev).manual_seed(11)
+    x = torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16)
+    x[::100] *= 50
+    w = torch.randn(K, N, device=dev, generator=g) / K ** 0.5
+    dy = (torch.randn(M, N, device=dev, generator=g) * 1e-3).to(torch.bfloat16)
+    xc = torch.empty(M, K, dtype=torch.uint8, device=dev)
+    wc = torch.empty(K, N, dtype=torch.uint8, device=dev)
+    sx = torch.empty(1, dtype=torch.int16, device=dev)
+    sw = torch.empty(1, dtype=torch.int16, device=dev)
+    amax = torch.empty(1, dtype=torch.int32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    xd = torch.empty(M, K, dtype=torch.bfloat16, device=dev)
+    wd = torch.empty(K, N, dtype=torch.bfloat16, device=dev)
+    y = torch.empty(M, N, dtype=torch.float32, device=dev)
+    dx = torch.empty(M, K, dtype=torch.bfloat16, device=dev)
+    dw = torch.empty(K, N, dtype=torch.float32, device=dev)
+    names = ["quant", "fwd", "dgrad", "wgrad"]
+    ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in names}
+
+    def step(rec=False):
+        s = st.cuda_stream
+        r = lambda k, i: ev[k][i].record(st) if rec else None
+        r("quant", 0)
+        for src, dt, rows, cols, codes, scale in ((x, 1, M, K, xc, sx), (w, 0, K, N, wc, sw)):
+            assert L.coat_group_scale_max(src.data_ptr(), dt, rows, cols, 128, None, amax.data_ptr(), s) == 0
+            assert L.coat_quantize_per_tensor(src.data_ptr(), dt, rows * cols, amax.data_ptr(), codes.data_ptr(),
+                                              scale.data_ptr(), flags.data_ptr(), s) == 0
+        assert L.coat_decode_e4m3_bf16(xc.data_ptr(), xd.data_ptr(), M * K, s) == 0
+        assert L.coat_decode_e4m3_bf16(wc.data_ptr(), wd.data_ptr(), K * N, s) == 0
+        r("quant", 1)
+        r("fwd", 0)
+        assert L.coat_fp8_linear_fwd(xc.data_ptr(), sx.data_ptr(), wc.data_ptr(), sw.data_ptr(), M, K, N,
+                                     y.data_ptr(), s) == 0, L.coat_last_error()
+        r("fwd", 1)
+        r("dgrad", 0)
+        assert L.coat_linear_bwd_dgrad(dy.data_ptr(), wd.data_ptr(), sw.data_ptr(), M, K, N, dx.data_ptr(), s) == 0
+        r("dgrad", 1)
+        r("wgrad", 0)
+        assert L.coat_linear_bwd_wgrad(xd.data_ptr(), sx.data_ptr(), dy.data_ptr(), M, K, N, dw.data_ptr(), s) == 0
+        r("wgrad", 1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    per = {k: 0.0 for k in names}
+    sampler = ClockSampler(0)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        start.record(st)
+        for _ in range(args.steps):
+            step(rec=True)
+            torch.cuda.synchronize()
+            for k in names:
+                per[k] += ev[k][0].elapsed_time(ev[k][1]) / args.steps
+        end.record(st)
+        torch.cuda.synchronize()
+    flop = 2.0 * M * N * K
+    ms = sum(per.values())
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16_peak = float(json.load(f)["bf16_tflops"])
+        kind = "measured bf16 (cuBLAS burst); fp8 peak taken as 2x"
+    except Exception:
+        bf16_peak, kind = 1590.0, "fallback"
+    tf = {k: flop / (per[k] * 1e-3) / 1e12 for k in ("fwd", "dgrad", "wgrad")}
+    out = {
+        "metric": "Per-tensor FP8 linear fwd+bwd (cfg4), TFLOP/s", "value": 3 * flop / (ms * 1e-3) / 1e12,
+        "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "e4m3 fwd / bf16 bwd, fp32 acc",
+        "data": "synthetic",
+        "config": {"workload": "cfg4: Llama-2-13B MLP linear, 8192 tokens x 5120 x 13824, per-tensor E4M3",
+                   "M": M, "K": K, "N": N},
+        "per_phase_ms": per, "tflops": tf,
+        "roofline": {"bound": "tensor", "achieved": tf["fwd"], "peak": 2 * bf16_peak, "unit": "TFLOP/s",
+                     "frac": tf["fwd"] / (2 * bf16_peak), "traffic": None, "peak_kind": kind,
+                     "bwd_frac_of_bf16": {"dgrad": tf["dgrad"] / bf16_peak, "wgrad": tf["wgrad"] / bf16_peak}},
+        "clocks": sampler.summary(), "gpu_launches": 9 * args.steps,
     }
     print(json.dumps(out))
 

@@ -144,6 +144,27 @@ coat_status coat_adamw_dre_step_host(const float* w_host_in, float* w_host_out, 
                                      coat_moment_state v_out, const coat_adamw_config* cfg,
                                      int64_t t, uint32_t* d_flags, int64_t chunk, void* stream);
 
+/* ----------------------------------------------------------- FP8 linear -- */
+/* The reference's linear (flow.cpp:21-46, no public entry point; SURVEY.md 8(a)
+ * a18) on tcgen05/TMEM/TMA.  W is (K, N) row-major as in flow.hpp:44-47.
+ * Scales are the BF16 device scalars written by coat_quantize_per_tensor.
+ * Constraints: K % 16 == 0, N % 16 == 0, 16-byte aligned buffers. */
+/* y[M,N] (fp32) = DQ(x)[M,K] . DQ(W)[K,N] = (s_x s_w) * codes_x . codes_w */
+coat_status coat_fp8_linear_fwd(const uint8_t* x_codes, const uint16_t* d_sx, const uint8_t* w_codes,
+                                const uint16_t* d_sw, int64_t M, int64_t K, int64_t N, float* y,
+                                void* stream);
+/* dX[M,K] (bf16) = bf16(dY[M,N] . W_used^T), W_used = s_w * w_dec (flow.cpp:636);
+ * w_dec = coat_decode_e4m3_bf16(w_codes), exact. */
+coat_status coat_linear_bwd_dgrad(const uint16_t* dy_bf16, const uint16_t* w_dec_bf16,
+                                  const uint16_t* d_sw, int64_t M, int64_t K, int64_t N,
+                                  uint16_t* dx_bf16, void* stream);
+/* dW[K,N] (fp32) = X_used^T . dY, X_used = s_x * x_dec (flow.cpp:637, 360-395). */
+coat_status coat_linear_bwd_wgrad(const uint16_t* x_dec_bf16, const uint16_t* d_sx,
+                                  const uint16_t* dy_bf16, int64_t M, int64_t K, int64_t N,
+                                  float* dw, void* stream);
+/* decode_byte(code) as BF16 bits (exact: E4M3 values have <= 4 significant bits). */
+coat_status coat_decode_e4m3_bf16(const uint8_t* codes, uint16_t* out_bf16, int64_t n, void* stream);
+
 /* Test/diagnostic hook: count elements that took the literal (double pow)
  * fallback in DRE kernels into *d_counter (device u64); NULL disables. */
 coat_status coat_set_fallback_counter(unsigned long long* d_counter);

@@ -357,3 +357,16 @@ int oracle_generate(int kind, int64_t rows, int64_t cols, double frac, double sc
     }
     return ST_OK;
 }
+
+/* ------------------------------------------------------------ linear ---- */
+/* flow.cpp:21-33 matmul: a (m,k) times b (k,n), fp32 accumulation in p order,
+ * skipping a == 0 exactly as the reference does. */
+void oracle_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n, float* out) {
+    for (int64_t i = 0; i < m * n; ++i) out[i] = 0.0f;
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t p = 0; p < k; ++p) {
+            const float av = a[i * k + p];
+            if (av == 0.0f) continue;
+            for (int64_t j = 0; j < n; ++j) out[i * n + j] += av * b[p * n + j];
+        }
+}

@@ -60,6 +60,8 @@ void oracle_reference_adamw_step(float* w, float* m, float* v, const float* g, i
 int oracle_generate(int kind, int64_t rows, int64_t cols, double frac, double scale,
                     uint64_t seed, float* out);
 uint64_t oracle_splitmix64_at(uint64_t seed, uint64_t i); /* i-th output of SplitMix64(seed) */
+/* flow.cpp:21-33 */
+void oracle_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n, float* out);
 
 #ifdef __cplusplus
 }

@@ -97,6 +97,7 @@ class Oracle:
                                                   C.POINTER(C.c_int)], None)
             self._optk = self._fn("optimal_k", [C.c_double, C.POINTER(C.c_float),
                                                 C.POINTER(C.c_int)], None)
+            self._matmul = self._fn("matmul", [_f32p, _f32p, _i64, _i64, _i64, _f32p], None)
         else:
             self._quant = self._fn("quantize", [_f32p, _i64p, C.c_int, C.c_int, _i64, _u8p,
                                                 _f32p, C.POINTER(C.c_int64)])
@@ -276,6 +277,14 @@ class Oracle:
         else:
             _chk(self._gen(kind, np.array(shape, np.int64), len(shape), frac, scale, seed,
                            out.ravel()))
+        return out
+
+    def matmul(self, a, b):
+        """flow.cpp:21-33 (port only): sequential fp32 accumulation."""
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        out = np.empty((a.shape[0], b.shape[1]), np.float32)
+        self._matmul(a.ravel(), b.ravel(), a.shape[0], a.shape[1], b.shape[1], out.ravel())
         return out
 
     def round_bf16(self, x):

@@ -70,6 +70,10 @@ _SIGS = {
                                   MomentState, MomentState, C.POINTER(AdamWConfigC), _i64, _vp,
                                   _i64, _vp], _int),
     "coat_set_fallback_counter": ([_vp], _int),
+    "coat_fp8_linear_fwd": ([_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp], _int),
+    "coat_linear_bwd_dgrad": ([_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp], _int),
+    "coat_linear_bwd_wgrad": ([_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp], _int),
+    "coat_decode_e4m3_bf16": ([_vp, _vp, _i64, _vp], _int),
 }
 
 

@@ -514,6 +514,64 @@ def step(params: torch.Tensor, grads: torch.Tensor, slot: OptimizerSlot, cfg: Ad
     slot.step = t
 
 
+# ------------------------------------------------------------ FP8 linear ----
+# The reference's linear (flow.cpp:21-46) has no public entry point; these
+# follow its semantics on tcgen05 (gemm_tcgen05.cu).
+
+def _per_tensor(q: QuantizedTensor, what: str) -> None:
+    if q.geometry.mode != QuantMode.PerTensor or len(q.source_shape) != 2:
+        raise InvalidSpec(f"{what}: expected a 2-D per-tensor QuantizedTensor")
+
+
+def decode_e4m3_bf16(codes: torch.Tensor) -> torch.Tensor:
+    """decode_byte of every code as bfloat16 (exact)."""
+    codes = codes.contiguous()
+    out = torch.empty(codes.shape, dtype=torch.bfloat16, device=codes.device)
+    _check(L.coat_decode_e4m3_bf16(codes.data_ptr(), out.data_ptr(), codes.numel(), _stream()))
+    return out
+
+
+def fp8_linear(qx: QuantizedTensor, qw: QuantizedTensor) -> torch.Tensor:
+    """y = matmul(DQ(Q_t(x)), DQ(Q_t(W))) (flow.cpp:21-33, 548-552); W is (K, N)."""
+    _per_tensor(qx, "fp8_linear")
+    _per_tensor(qw, "fp8_linear")
+    (M, K), (K2, N) = qx.source_shape, qw.source_shape
+    if K != K2:
+        raise ShapeMismatch("fp8_linear: inner dimensions differ")
+    y = torch.empty(M, N, dtype=torch.float32, device=qx.codes.device)
+    _check(L.coat_fp8_linear_fwd(qx.codes.data_ptr(), qx.scales.data_ptr(), qw.codes.data_ptr(),
+                                 qw.scales.data_ptr(), M, K, N, y.data_ptr(), _stream()))
+    return y
+
+
+def linear_dgrad(dy: torch.Tensor, qw: QuantizedTensor, w_dec: torch.Tensor | None = None) -> torch.Tensor:
+    """dX = bf16(dY . W_used^T) (flow.cpp:636); dY is BF16 and not quantized."""
+    _per_tensor(qw, "linear_dgrad")
+    K, N = qw.source_shape
+    M = dy.shape[0]
+    if tuple(dy.shape) != (M, N) or dy.dtype != torch.bfloat16:
+        raise ShapeMismatch("linear_dgrad: dY must be bf16 (M, N)")
+    w_dec = decode_e4m3_bf16(qw.codes) if w_dec is None else w_dec
+    dx = torch.empty(M, K, dtype=torch.bfloat16, device=dy.device)
+    _check(L.coat_linear_bwd_dgrad(dy.contiguous().data_ptr(), w_dec.data_ptr(), qw.scales.data_ptr(), M, K, N,
+                                   dx.data_ptr(), _stream()))
+    return dx
+
+
+def linear_wgrad(qx: QuantizedTensor, dy: torch.Tensor, x_dec: torch.Tensor | None = None) -> torch.Tensor:
+    """dW = X_used^T . dY (flow.cpp:637 with used_values_transposed, 360-395)."""
+    _per_tensor(qx, "linear_wgrad")
+    M, K = qx.source_shape
+    N = dy.shape[1]
+    if tuple(dy.shape) != (M, N) or dy.dtype != torch.bfloat16:
+        raise ShapeMismatch("linear_wgrad: dY must be bf16 (M, N)")
+    x_dec = decode_e4m3_bf16(qx.codes) if x_dec is None else x_dec
+    dw = torch.empty(K, N, dtype=torch.float32, device=dy.device)
+    _check(L.coat_linear_bwd_wgrad(x_dec.data_ptr(), qx.scales.data_ptr(), dy.contiguous().data_ptr(), M, K, N,
+                                   dw.data_ptr(), _stream()))
+    return dw
+
+
 def set_fallback_counter(counter: torch.Tensor | None) -> None:
     """Diagnostics: count literal-formula fallbacks of the DRE kernels."""
     _check(L.coat_set_fallback_counter(None if counter is None else counter.data_ptr()))

@@ -415,3 +415,19 @@ cudaError_t launch_quantize_per_tensor(const void* x, int dtype, int64_t n, cons
 }
 
 }  // namespace coat
+
+namespace coat {
+namespace {
+__global__ void decode_bf16_kernel(const uint8_t* __restrict__ c, uint16_t* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = uint16_t(f2u(e4m3_decode(c[i])) >> 16);   // exact: <= 4 significant bits
+}
+}  // namespace
+
+cudaError_t launch_decode_e4m3_bf16(const uint8_t* codes, uint16_t* out, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = imin64((n + 255) / 256, int64_t(device_sm_count()) * 8);
+    decode_bf16_kernel<<<int(blocks), 256, 0, st>>>(codes, out, n);
+    return cudaGetLastError();
+}
+}  // namespace coat

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <climits>
 #include <mutex>
 
 #include "../../include/coat.h"
@@ -223,6 +224,47 @@ coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g,
     if (!w_in || !w_out || !g) return fail(COAT_ERR_INVALID, "step: NULL buffer");
     return cuda_status(launch_adamw_dre_step(w_in, w_out, g, n, in_of(m_in), in_of(v_in), out_of(m_out),
                                              out_of(v_out), a, d_flags, g_fallback_counter, S(stream)));
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ FP8 linear -----
+extern "C" {
+
+static coat_status check_linear(int64_t M, int64_t K, int64_t N, const void* a, const void* b, const void* out) {
+    if (M <= 0 || K <= 0 || N <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (M > INT32_MAX || K > INT32_MAX || N > INT32_MAX) return fail(COAT_ERR_INVALID, "dimension too large");
+    if (K % 16 != 0 || N % 16 != 0) return fail(COAT_ERR_SHAPE, "linear: K and N must be multiples of 16 (TMA strides)");
+    if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out)) & 15u)
+        return fail(COAT_ERR_INVALID, "linear: buffers must be 16-byte aligned");
+    return COAT_OK;
+}
+
+coat_status coat_fp8_linear_fwd(const uint8_t* x_codes, const uint16_t* d_sx, const uint8_t* w_codes,
+                                const uint16_t* d_sw, int64_t M, int64_t K, int64_t N, float* y, void* stream) {
+    const coat_status st = check_linear(M, K, N, x_codes, w_codes, y);
+    if (st != COAT_OK) return st;
+    return cuda_status(launch_fp8_linear_fwd(x_codes, d_sx, w_codes, d_sw, int(M), int(K), int(N), y, S(stream)));
+}
+
+coat_status coat_linear_bwd_dgrad(const uint16_t* dy_bf16, const uint16_t* w_dec_bf16, const uint16_t* d_sw,
+                                  int64_t M, int64_t K, int64_t N, uint16_t* dx_bf16, void* stream) {
+    const coat_status st = check_linear(M, K, N, dy_bf16, w_dec_bf16, dx_bf16);
+    if (st != COAT_OK) return st;
+    return cuda_status(launch_linear_dgrad(dy_bf16, w_dec_bf16, d_sw, int(M), int(K), int(N), dx_bf16, S(stream)));
+}
+
+coat_status coat_linear_bwd_wgrad(const uint16_t* x_dec_bf16, const uint16_t* d_sx, const uint16_t* dy_bf16,
+                                  int64_t M, int64_t K, int64_t N, float* dw, void* stream) {
+    const coat_status st = check_linear(M, K, N, x_dec_bf16, dy_bf16, dw);
+    if (st != COAT_OK) return st;
+    if (M % 16 != 0) return fail(COAT_ERR_SHAPE, "wgrad: M must be a multiple of 16 (TMA strides)");
+    return cuda_status(launch_linear_wgrad(x_dec_bf16, d_sx, dy_bf16, int(M), int(K), int(N), dw, S(stream)));
+}
+
+coat_status coat_decode_e4m3_bf16(const uint8_t* codes, uint16_t* out_bf16, int64_t n, void* stream) {
+    if (n < 0) return fail(COAT_ERR_INVALID, "decode: negative n");
+    return cuda_status(launch_decode_e4m3_bf16(codes, out_bf16, n, S(stream)));
 }
 
 }  // extern "C"

@@ -59,6 +59,15 @@ cudaError_t host_pipelined_step(const float* w_host_in, float* w_host_out, const
                                 const AdamWScalars& a, uint32_t* flags, unsigned long long* fallbacks,
                                 int64_t chunk, cudaStream_t stream);
 
+// tcgen05 GEMMs (gemm_tcgen05.cu)
+cudaError_t launch_fp8_linear_fwd(const uint8_t* xc, const uint16_t* sx, const uint8_t* wc, const uint16_t* sw, int M,
+                                  int K, int N, float* y, cudaStream_t st);
+cudaError_t launch_linear_dgrad(const uint16_t* dy, const uint16_t* wd, const uint16_t* sw, int M, int K, int N,
+                                uint16_t* dx, cudaStream_t st);
+cudaError_t launch_linear_wgrad(const uint16_t* xd, const uint16_t* sx, const uint16_t* dy, int M, int K, int N,
+                                float* dw, cudaStream_t st);
+cudaError_t launch_decode_e4m3_bf16(const uint8_t* codes, uint16_t* out, int64_t n, cudaStream_t st);
+
 // activation quantizers (act_quant.cu)
 cudaError_t launch_encode_e4m3(const float* x, uint8_t* out, int64_t n, uint32_t* flags,
                                cudaStream_t stream);

@@ -1,0 +1,107 @@
+"""GPU parity: the per-tensor FP8 linear (K4, tcgen05/TMEM/TMA) and its BF16
+backward GEMMs.
+
+Reference: flow.cpp:21-33 (matmul, sequential fp32 accumulation), 36-46
+(matmul_nt), 548-552/636-637 (call sites), 360-395 (transposed FP8 codes).
+Tolerance: |y - y_ref| <= tau * sum_p |a_ip b_pj|; E4M3 x
+E4M3 products are exact in fp32, so the only differences are accumulation
+order/precision.  tau is stated per test and the measured value printed.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TAU = 2.0 ** -16   # fp32 accumulation over K <= 5120 terms, order-independent bound
+
+
+def _quant_pair(coat, M, K, N, seed):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(M, K, device="cuda", generator=g)
+    x[:: 37] *= 50.0                           # outlier token rows (ActivationWithOutliers)
+    w = torch.randn(K, N, device="cuda", generator=g) / K ** 0.5
+    qx = coat.quantize(x.to(torch.bfloat16), coat.QuantGeometry.per_tensor())
+    qw = coat.quantize(w, coat.QuantGeometry.per_tensor())
+    return qx, qw
+
+
+def _ratio(y, ref, bound):
+    import torch
+    err = (y.double() - ref).abs()
+    return float((err / bound.clamp_min(1e-300)).max())
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 256, 256), (200, 272, 400), (512, 1024, 768), (384, 5120, 13824)])
+def test_fp8_linear_forward(coat, M, K, N):
+    import torch
+    qx, qw = _quant_pair(coat, M, K, N, seed=M + N)
+    y = coat.fp8_linear(qx, qw)
+    torch.cuda.synchronize()
+    a = coat.decode_e4m3(qx.codes).double()
+    b = coat.decode_e4m3(qw.codes).double()
+    s = float(qx.scales.float()) * float(qw.scales.float())
+    ref = (a @ b) * s
+    bound = (a.abs() @ b.abs()) * s * TAU + 1e-30
+    r = _ratio(y, ref, bound)
+    print(f"fp8_linear {M}x{K}x{N}: max err / (tau*sum|ab|) = {r:.3g}")
+    assert r <= 1.0
+
+
+def test_fp8_linear_matches_reference_loop(coat, port):
+    """Against the C restatement of flow.cpp:21-33 (sequential fp32 loop)."""
+    import torch
+    M, K, N = 128, 512, 256
+    qx, qw = _quant_pair(coat, M, K, N, seed=5)
+    y = coat.fp8_linear(qx, qw).cpu().numpy()
+    xd = coat.dequantize(qx).cpu().numpy()
+    wd = coat.dequantize(qw).cpu().numpy()
+    ref = port.matmul(xd, wd)
+    bound = np.abs(xd).astype(np.float64) @ np.abs(wd).astype(np.float64)
+    ratio = np.max(np.abs(y.astype(np.float64) - ref) / np.maximum(bound * TAU, 1e-300))
+    print("vs reference loop:", ratio)
+    assert ratio <= 1.0
+    assert np.mean(y == ref) > 0.05   # many outputs bit-identical to the sequential loop
+
+
+def test_linear_dgrad(coat):
+    import torch
+    M, K, N = 256, 512, 768
+    qx, qw = _quant_pair(coat, M, K, N, seed=11)
+    g = torch.Generator(device="cuda").manual_seed(13)
+    dy = (torch.randn(M, N, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
+    dx = coat.linear_dgrad(dy, qw)
+    torch.cuda.synchronize()
+    wu = coat.dequantize(qw).double()                          # W_used (K, N)
+    ref = dy.double() @ wu.t()
+    bound = (dy.double().abs() @ wu.abs().t()) * TAU
+    err = (dx.double() - ref).abs()
+    ok = err <= ref.abs() * 2.0 ** -8 + bound + 1e-30          # bf16 output rounding + accumulation
+    assert bool(ok.all()), float((err - ref.abs() * 2.0 ** -8).max())
+
+
+def test_linear_wgrad(coat):
+    import torch
+    M, K, N = 384, 256, 512
+    qx, qw = _quant_pair(coat, M, K, N, seed=17)
+    g = torch.Generator(device="cuda").manual_seed(19)
+    dy = (torch.randn(M, N, device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
+    dw = coat.linear_wgrad(qx, dy)
+    torch.cuda.synchronize()
+    xu = coat.dequantize(qx).double()                          # X_used (M, K)
+    ref = xu.t() @ dy.double()
+    bound = (xu.abs().t() @ dy.double().abs()) * TAU + 1e-30
+    r = _ratio(dw, ref, bound)
+    print("wgrad ratio", r)
+    assert r <= 1.0
+
+
+def test_linear_errors(coat):
+    import torch
+    qx, qw = _quant_pair(coat, 128, 256, 256, seed=1)
+    qbad = coat.quantize(torch.randn(128, 128, device="cuda"), coat.QuantGeometry.per_tensor())
+    with pytest.raises(coat.ShapeMismatch):
+        coat.fp8_linear(qx, qbad)
+    qg = coat.quantize(torch.randn(128, 256, device="cuda"), coat.QuantGeometry.per_group(16))
+    with pytest.raises(coat.InvalidSpec):
+        coat.fp8_linear(qg, qw)
