@@ -27,6 +27,7 @@
 // (ping-pong), so the host commits exactly what the reference would have
 // committed (see paper_2410_19313_b200/coatsim.py: step()).
 #include <cstdint>
+#include <cstdlib>
 
 #include "coat_device.cuh"
 #include "dre.cuh"
@@ -399,7 +400,13 @@ cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* 
     int64_t done = 0;
     if (!fallbacks) {
         const int64_t nfull = n / kTile;
-        const cudaError_t e = launch_k1_fast(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream);
+        // COAT_K1=v2 selects the previous (per-warp) kernel, for A/B measurement
+        static const bool use_v2 = [] {
+            const char* s = getenv("COAT_K1");
+            return s && s[0] == 'v' && s[1] == '2';
+        }();
+        const cudaError_t e = use_v2 ? launch_k1_fast(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream)
+                                     : launch_k1_ws(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream);
         if (e == cudaSuccess) done = nfull * kTile;
         else if (e != cudaErrorNotSupported) return e;
     }

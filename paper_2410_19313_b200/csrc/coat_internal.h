@@ -38,6 +38,10 @@ cudaError_t launch_k1_fast(const float* w_in, float* w_out, const float* g, int6
                            const MomentStateIn& m_in, const MomentStateIn& v_in, const MomentStateOut& m_out,
                            const MomentStateOut& v_out, const AdamWScalars& a, uint32_t* flags,
                            cudaStream_t stream);
+cudaError_t launch_k1_ws(const float* w_in, float* w_out, const float* g, int64_t ntiles,
+                         const MomentStateIn& m_in, const MomentStateIn& v_in, const MomentStateOut& m_out,
+                         const MomentStateOut& v_out, const AdamWScalars& a, uint32_t* flags,
+                         cudaStream_t stream);
 cudaError_t launch_expand_quantize_fast(const float* x, int64_t ntiles, const MomentStateOut& out,
                                         double log_target, uint32_t* flags, cudaStream_t stream);
 cudaError_t launch_dequantize_contract_fast(const MomentStateIn& in, int64_t ntiles, float* x, uint32_t* flags,

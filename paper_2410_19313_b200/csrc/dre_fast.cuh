@@ -8,16 +8,18 @@
 //       T1[jj] = jj^(1/k) (negated in the upper half),
 //       T2[ee] = c * s^(1/k) * 2^((ee-10)/k).
 //   The tables (48 doubles per (group, moment)) are built once per tile by 4
-//   lanes with a double-precision exp2 (64-entry table + degree-5 polynomial,
-//   no SFU).  Each element then costs two LDS.64, one DMUL, one F2F and -- for
-//   k != 1 -- a 3-op certification of the float rounding; the ~2e-6 uncertain
-//   elements take the literal reference formula behind a warp vote.  For k == 1
-//   every product is exact in double, so no certification is needed.
+//   lanes in UNIFORM SIMT rounds (every lane evaluates the same double exp2 on
+//   its own argument: primes of jj, three T2 anchors; products for the rest),
+//   so a warp builds its 8 tables with 3 exp2 rounds.  Each element then costs
+//   two LDS.64, one DMUL, one F2F and -- for k != 1 -- a 2-op certification of
+//   the float rounding; the ~2e-6 uncertain elements take the literal
+//   reference formula behind a warp vote.  For k == 1 every product is exact
+//   in double, so no certification is needed.
 //
 // Expand + encode (expand.cpp:18-22, quantize.cpp:19-27):
-//   e = (|x|/c)^k on the SFU (lg2/ex2.approx) or |x|*RN(1/c) for k == 1;
-//   code = E4M3(e/s) is certified by encoding both ends of an error interval
-//   with one cvt.e4m3x2 (certified_code in coat_device.cuh).
+//   k == 1: e = RN(|x|/c), q = RN(e/s) exactly (Markstein); else e = (|x|/c)^k
+//   on the SFU (lg2/ex2.approx) and the E4M3 code of e/s certified by encoding
+//   both ends of an error interval with one cvt.e4m3x2.
 #pragma once
 
 #include "coat_device.cuh"
@@ -68,8 +70,20 @@ struct PairContract {
     int exact;       // 1: k == 1, products exact, no certification needed
 };
 
-// Lane q (0..3) of the 4 lanes serving one (group, moment) builds entries
-// 4q..4q+3.  Must be called by all 32 lanes of the warp together.
+__device__ __forceinline__ double sel4(int q, double a, double b, double c, double d) {
+    return q == 0 ? a : q == 1 ? b : q == 2 ? c : d;
+}
+
+// Lane q (0..3) of the 4 lanes serving one (group, moment); must be called by
+// all 32 lanes of the warp together (8 pairs x 4 lanes, convergent).  Every
+// step below is the same instruction stream on all lanes (no divergence):
+//   round 1: T1[{2,3,5,7}[q]]           = exp2(ik * log2 p)
+//   round 2: T1[11], T1[13], T2[1], T2[5] = exp2(...)     (q = 0..3)
+//   round 3: T2[9], T2[13]                = exp2(...)     (q = 0, 1; 2, 3 idle)
+//   products: T1 composites from the primes, T2[e+1..e+3] = T2[e] * u^(1..3)
+// Entries are within ~2^-49 of the exact values (<= 4 roundings after exp2),
+// well inside the 2^-43 certification margin.  For k == 1 every entry is set
+// exactly (T1[j] = j, T2[e] = c*s*2^(e-10)).
 __device__ __forceinline__ void build_pair_contract(PairContract& P, int q, float s, float k, float c,
                                                     const CtaTables& T, int lane) {
     const double cd = (double)c;
@@ -77,30 +91,56 @@ __device__ __forceinline__ void build_pair_contract(PairContract& P, int q, floa
     bool odd = !(s >= 0x1p-100f) || !(s <= 0x1p100f) || !(c > 0.0f) || !(c <= 3.0e38f) ||
                !(k >= 1.0f) || !(k <= 20.0f);
     const bool exact = (k == 1.0f);
-    double ik = 1.0, l2s = 0.0, cs = 0.0;
-    if (exact) {
-        cs = cd * (double)s;   // exact: 24 x 8 significant bits
+    const double ik = exact ? 1.0 : 1.0 / (double)k;
+    const double l2s = (double)(int((sb >> 23) & 0xFFu) - 127) + T.l2b[(sb >> 16) & 0x7Fu];
+    const double cs = cd * (double)s;          // exact product (24 x 8 bits)
+
+    // ---- round 1: primes 2, 3, 5, 7
+    const int p1 = q == 0 ? 2 : q == 1 ? 3 : q == 2 ? 5 : 7;
+    const double v1 = exact ? (double)p1 : exp2_fast(ik * T.l2j[p1], T);
+    // ---- round 2: T1[11], T1[13], T2[1], T2[5]
+    const double e2 = sel4(q, T.l2j[11], T.l2j[13], l2s - 9.0, l2s - 5.0);
+    double v2 = exp2_fast(ik * e2, T);
+    if (q >= 2) v2 *= cd;
+    const double x2 = sel4(q, 11.0, 13.0, cs * 0x1p-9, cs * 0x1p-5);   // exact values for k == 1
+    v2 = exact ? x2 : v2;
+    // ---- round 3: T2[9], T2[13]
+    const double e3 = q == 0 ? l2s - 1.0 : l2s + 3.0;
+    double v3 = cd * exp2_fast(ik * e3, T);
+    v3 = exact ? (q == 0 ? cs * 0.5 : cs * 8.0) : v3;
+    P.t1[p1] = v1;
+    if (q < 2) {
+        P.t1[q == 0 ? 11 : 13] = v2;
+        P.t2[q == 0 ? 9 : 13] = v3;
     } else {
-        ik = 1.0 / (double)k;
-        l2s = (double)(int((sb >> 23) & 0xFFu) - 127) + T.l2b[(sb >> 16) & 0x7Fu];
+        P.t2[q == 2 ? 1 : 5] = v2;
     }
-#pragma unroll 1
-    for (int t = 0; t < 4; ++t) {
-        const int i = 4 * q + t;
-        double a, b;
-        if (exact) {
-            // pow(|y|, 1.0) == |y|: X = jj * (c * s * 2^(ee-10)) exactly.
-            a = (double)i;
-            b = cs * __hiloint2double((1023 + i - 10) << 20, 0);
-        } else {
-            a = exp2_fast(ik * T.l2j[i], T);
-            b = cd * exp2_fast(ik * (l2s + (double)(i - 10)), T);
-        }
-        if (i == 0) a = b = 0.0;
-        P.t1[i] = a;
-        P.t1[16 + i] = -a;
-        P.t2[i] = b;
+    __syncwarp();
+    // ---- products
+    const double u = P.t1[2];                  // 2^(1/k)
+    const double t3 = P.t1[3], t5 = P.t1[5], t7 = P.t1[7];
+    // T1 composites (2 per lane): 4 6 | 8 9 | 10 12 | 14 15 ; T1[0] = 0, T1[1] = 1
+    const int d0 = q == 0 ? 4 : q == 1 ? 8 : q == 2 ? 10 : 14;
+    const int d1 = q == 0 ? 6 : q == 1 ? 9 : q == 2 ? 12 : 15;
+    const double c0 = q == 0 ? u * u : q == 1 ? (u * u) * u : q == 2 ? u * t5 : u * t7;
+    const double c1 = q == 0 ? u * t3 : q == 1 ? t3 * t3 : q == 2 ? (u * u) * t3 : t3 * t5;
+    P.t1[d0] = c0;
+    P.t1[d1] = c1;
+    // T2 chain from the anchors T2[1], T2[5], T2[9], T2[13] (lane q: anchor 4q+1)
+    const double anchor = P.t2[4 * q + 1];
+    const double a1 = anchor * u, a2 = a1 * u, a3 = a2 * u;
+    P.t2[4 * q + 2] = a1;
+    P.t2[4 * q + 3] = a2;
+    if (q < 3) P.t2[4 * q + 4] = a3;
+    if (q == 0) {
+        P.t1[0] = 0.0;
+        P.t1[1] = 1.0;
+        P.t2[0] = 0.0;
     }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 4; ++t) P.t1[16 + 4 * q + t] = -P.t1[4 * q + t];
+    __syncwarp();
     P.t1[16] = 0.0;   // code 0x80: contract_one returns +0
     // Nonzero |X| spans [T1[1]*T2[1], T1[14]*T2[15]] (codes 0x01 .. 0x7E): keep
     // every product in the fp32 normal range or send the whole pair to the
@@ -129,15 +169,17 @@ __device__ __forceinline__ void contract_word(uint32_t codes, const PairContract
     const uint32_t nz = ((expf + 0x0F0F0F0Fu) & 0x10101010u) >> 1;   // 0x08 where expf != 0
     const uint32_t jj = (mag & 0x07070707u) | nz | ((codes >> 3) & 0x10101010u);
     const uint32_t ee = expf | ((~nz >> 3) & 0x01010101u);            // max(expf, 1)
-    uint32_t near = 0;
+    // distance of the low 29 mantissa bits from the float midpoint 2^28, times 8
+    // (the multiply shifts the 3 bits above bit 28 out): min over the 4 elements
+    uint32_t near = 0xFFFFFFFFu;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const double X = P.t1[(jj >> (8 * i)) & 0xFFu] * P.t2[(ee >> (8 * i)) & 0xFFu];
-        // within 512 double-ulps of a float rounding midpoint?
-        near |= (((uint32_t)__double2loint(X) - 0x0FFFFE00u) & 0x1FFFFFFFu) < 0x400u ? (1u << i) : 0u;
+        near = min(near, ((uint32_t)__double2loint(X) - 0x0FFFFE00u) * 8u);
         x[i] = __double2float_rn(X);
     }
-    unsure |= P.literal ? 0xFu : (P.exact ? 0u : near);
+    // any element within 512 double-ulps of a midpoint -> recompute all 4 (rare)
+    unsure |= (P.literal || (!P.exact && near < 0x400u * 8u)) ? 0xFu : 0u;
 }
 
 // Parameters of a NEW (group, moment) state: measure_group + optimal_k + the
@@ -222,28 +264,20 @@ __device__ __forceinline__ uint32_t pack_word(const float (&x)[4], const PackPar
         return c2[0] | (c2[1] << 16);
     }
     F2 q[2];
-    const float rel = p.mode == 0 ? kRelLinear : kRelMufu;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const F2 ax{fabsf(x[2 * h]), fabsf(x[2 * h + 1])};
         const F2 r = f2_mul(ax, f2s(p.inv_c), nz);
-        F2 e;
-        if (p.mode == 0) {
-            e = r;
-        } else {
-            const F2 l{lg2_approx(r.x), lg2_approx(r.y)};
-            const F2 u = f2_mul(l, f2s(p.k), nz);
-            e = F2{ex2_approx(u.x), ex2_approx(u.y)};
-        }
-        const F2 qq = f2_mul(e, f2s(p.inv_s), nz);
+        const F2 l{lg2_approx(r.x), lg2_approx(r.y)};
+        const F2 u = f2_mul(l, f2s(p.k), nz);
+        const F2 qq = f2_mul(F2{ex2_approx(u.x), ex2_approx(u.y)}, f2s(p.inv_s), nz);
         q[h] = F2{u2f(f2u(qq.x) | (f2u(x[2 * h]) & 0x80000000u)), u2f(f2u(qq.y) | (f2u(x[2 * h + 1]) & 0x80000000u))};
     }
-    const F2 lo01 = f2_mul(q[0], f2s(1.0f - rel), nz), hi01 = f2_mul(q[0], f2s(1.0f + rel), nz);
-    const F2 lo23 = f2_mul(q[1], f2s(1.0f - rel), nz), hi23 = f2_mul(q[1], f2s(1.0f + rel), nz);
+    const F2 lo01 = f2_mul(q[0], f2s(1.0f - kRelMufu), nz), hi01 = f2_mul(q[0], f2s(1.0f + kRelMufu), nz);
+    const F2 lo23 = f2_mul(q[1], f2s(1.0f - kRelMufu), nz), hi23 = f2_mul(q[1], f2s(1.0f + kRelMufu), nz);
     const uint32_t c01 = cvt_e4m3x2(lo01.x, lo01.y), d01 = cvt_e4m3x2(hi01.x, hi01.y);
     const uint32_t c23 = cvt_e4m3x2(lo23.x, lo23.y), d23 = cvt_e4m3x2(hi23.x, hi23.y);
-    unsure |= (c01 != d01 ? 0x3u : 0u) | (c23 != d23 ? 0xCu : 0u);
-    if (p.mode == 2) unsure = 0xFu;
+    unsure |= (c01 != d01 ? 0x3u : 0u) | (c23 != d23 ? 0xCu : 0u) | (p.mode == 2 ? 0xFu : 0u);
     return c01 | (c23 << 16);
 }
 
