@@ -12,7 +12,8 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcoat.so")
+# COAT_LIB: A/B measurement of alternative builds of the same sources (tools/ab.sh)
+LIB_PATH = os.environ.get("COAT_LIB") or os.path.join(HERE, "libcoat.so")
 
 COAT_OK = 0
 STATUS_NAMES = {

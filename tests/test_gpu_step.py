@@ -85,6 +85,37 @@ def test_step_from_warmed_state(coat, port):
     run_both(coat, port, n, 3, warm=warm)
 
 
+def test_step_sparse_zero_and_extreme_groups(coat, port):
+    """Groups the fast paths must hand off exactly: whole zero groups (v' == 0,
+    all-zero state), scattered zero gradients (zero-aware extrema), tiny and
+    huge gradient groups (IEEE AdamW path, literal contract/pack), through
+    several steps so k == 1 and k > 1 states both reach the contract."""
+    n = 96 * 2048 + 640
+    w0 = port.generate(0, (n,), 0.0, 100.0, 5) * np.float32(0.02)
+    w_ref = w0.copy()
+    m, v = port.make_slot(n)
+    slot = coat.make_slot([n])
+    w = dev(w0)
+    c = coat.AdamWConfig(**CFG)
+    r = rng(77)
+    for t in range(6):
+        g = port.generate(0, (n,), 0.01, 100.0, 300 + t) * np.float32(1e-3)
+        gv = g.reshape(-1, 128)
+        gv[r.random(gv.shape[0]) < 0.15] = 0.0                    # untouched rows
+        gv[r.random(gv.shape) < 0.05] = 0.0                       # scattered zeros
+        gv[3::41] *= np.float32(1e-30)                            # tiny groups
+        gv[5::53] *= np.float32(1e16)                             # huge groups
+        gv[7::59, :64] = 0.0
+        assert port.step(w_ref, g, m, v, t, CFG) == 0
+        coat.step(w, dev(g), slot, c)
+        gm, gvs = gpu_state(slot)
+        wd = host(w)
+        bad = np.nonzero(wd.view(np.uint32) != w_ref.view(np.uint32))[0]
+        assert bad.size == 0, (t, bad[:8], wd[bad[:8]], w_ref[bad[:8]])
+        assert_state_equal(gm, m, f"m step {t}")
+        assert_state_equal(gvs, v, f"v step {t}")
+
+
 def test_step_without_weight_decay_and_large_grads(coat, port):
     run_both(coat, port, 1 << 14, 3, cfg=dict(CFG, weight_decay=0.0), grad_scale=1.0)
 
