@@ -471,14 +471,9 @@ def make_slot(shape, policy: SlotPolicy | None = None, device="cuda") -> Optimiz
     return slot
 
 
-def step(params: torch.Tensor, grads: torch.Tensor, slot: OptimizerSlot, cfg: AdamWConfig,
-         check: bool = True) -> None:
-    """optimizer.hpp:58: one fused kernel; then commit like the reference.
-
-    * NonFiniteGradient (optimizer.cpp:104): nothing is mutated.
-    * NonFiniteInput from pack_moment(m): params updated, slot unchanged.
-    * NonFiniteInput from pack_moment(v): params and slot.m updated, v and step not.
-    """
+def _step_launch(params: torch.Tensor, grads: torch.Tensor, slot: OptimizerSlot, cfg: AdamWConfig) -> None:
+    """Validate (before any mutation, like optimizer.cpp:102-104) and launch the
+    fused kernel into the slot's spare buffers; nothing is committed yet."""
     if tuple(params.shape) != slot.shape:
         raise ShapeMismatch("step: params do not match slot shape")
     if tuple(grads.shape) != tuple(params.shape):
@@ -499,19 +494,38 @@ def step(params: torch.Tensor, grads: torch.Tensor, slot: OptimizerSlot, cfg: Ad
     _check(L.coat_adamw_dre_step(params.data_ptr(), slot._w_scratch.data_ptr(), grads.data_ptr(),
                                  n, DRE_GROUP, mi.c_struct(), vi.c_struct(), mo.c_struct(),
                                  vo.c_struct(), C.byref(c), t, slot._flags.ptr, _stream()))
-    flags = slot._flags.value() if check else 0
+
+
+def _step_commit(params: torch.Tensor | None, slot: OptimizerSlot, flags: int) -> None:
+    """Commit a launched step exactly as the reference would have (optimizer.cpp:101-114):
+
+    * NonFiniteGradient (optimizer.cpp:104): nothing is mutated.
+    * NonFiniteInput from unpack (contract): nothing is mutated.
+    * NonFiniteInput from pack_moment(m): params updated, slot unchanged.
+    * NonFiniteInput from pack_moment(v): params and slot.m updated, v and step not.
+    params=None: the caller publishes slot._w_scratch itself (ZeRO all-gather).
+    """
     if flags & _lib.FLAG_NONFINITE_GRAD:
         raise NonFiniteGradient("step: gradient has non-finite values")
     if flags & _lib.FLAG_CONTRACT:
         raise NonFiniteInput("contract: tensor has non-finite values")
-    params.copy_(slot._w_scratch)
+    if params is not None:
+        params.copy_(slot._w_scratch)
     if flags & _lib.FLAG_PACK_M:
         raise NonFiniteInput("expand_quantize: tensor has non-finite values")
     slot._cm = 1 - slot._cm
     if flags & _lib.FLAG_PACK_V:
         raise NonFiniteInput("expand_quantize: tensor has non-finite values")
     slot._cv = 1 - slot._cv
-    slot.step = t
+    slot.step = slot.step + 1
+
+
+def step(params: torch.Tensor, grads: torch.Tensor, slot: OptimizerSlot, cfg: AdamWConfig,
+         check: bool = True) -> None:
+    """optimizer.hpp:58: one fused kernel (K1), then commit like the reference
+    (see _step_commit for the error semantics)."""
+    _step_launch(params, grads, slot, cfg)
+    _step_commit(params, slot, slot._flags.value() if check else 0)
 
 
 # ------------------------------------------------------------ FP8 linear ----

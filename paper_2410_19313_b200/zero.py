@@ -1,0 +1,186 @@
+"""ZeRO-sharded FP8-DRE AdamW over torch.distributed (one process per GPU).
+
+The reference steps one tensor at a time (coatsim::step, optimizer.cpp:101-114)
+and has no distributed code.  Its Dynamic Range Expansion statistics are per
+1x128 group (expand.cpp:57-83), so a flat buffer whose tensors each start on a
+128-element boundary can be cut into 128-aligned shards that are stepped
+independently, bit for bit equal to the per-tensor reference step
+("shard independence"; tests/test_zero.py checks
+it with the oracle on 2 gloo ranks).
+
+Per step, rank r:
+  1. reduce-scatter of the full fp32 gradient buffer (sum) -> its shard,
+  2. the fused K1 kernel (coatsim._step_launch) on its shard of the weights
+     and its shard of the FP8-DRE state (the state is never communicated); the
+     new weight shard goes to a scratch buffer,
+  3. an all-reduce of the 5-bit error word, so every rank commits exactly
+     what the single-process step would commit for the union of the shards
+     (coatsim._step_commit: NonFiniteGradient anywhere -> nothing changes
+     anywhere),
+  4. when the weights change: all-gather of the scratch shards straight into
+     the full weight buffer -- the all-gather IS the commit, so the sharded
+     step moves no extra bytes (world size 1: one copy).
+
+NCCL over NVLink on B200 (``backend="nccl"``); the same code runs on gloo for
+the CPU tests of the plumbing.  Gradient averaging is the caller's choice
+(``grad_op="sum"`` like the reference, which just consumes g).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import _lib, coatsim
+
+GROUP = coatsim.DRE_GROUP
+
+
+def _round_up(x: int, m: int) -> int:
+    return -(-x // m) * m
+
+
+@dataclass(frozen=True)
+class FlatLayout:
+    """Tensors packed into one flat fp32 buffer, each padded to a multiple of
+    128 elements (optimizer.cpp:24-38 pad_flat), the total padded to a
+    multiple of 128 * world_size so every rank owns an equal 128-aligned shard."""
+
+    shapes: tuple
+    offsets: tuple
+    numels: tuple
+    total: int
+    world_size: int
+
+    @staticmethod
+    def build(shapes: Sequence[Sequence[int]], world_size: int = 1) -> "FlatLayout":
+        if world_size < 1:
+            raise coatsim.InvalidSpec("world_size must be >= 1")
+        offs, numels, cur = [], [], 0
+        norm = []
+        for s in shapes:
+            s = tuple(int(d) for d in s)
+            if any(d <= 0 for d in s):
+                raise coatsim.InvalidSpec("tensor dimensions must be positive")
+            n = 1
+            for d in s:
+                n *= d
+            norm.append(s)
+            offs.append(cur)
+            numels.append(n)
+            cur += _round_up(n, GROUP)
+        total = _round_up(max(cur, 1), GROUP * world_size)
+        return FlatLayout(tuple(norm), tuple(offs), tuple(numels), total, world_size)
+
+    @property
+    def shard_numel(self) -> int:
+        return self.total // self.world_size
+
+    def shard(self, rank: int) -> tuple[int, int]:
+        lo = rank * self.shard_numel
+        return lo, lo + self.shard_numel
+
+    def flatten(self, tensors: Sequence[torch.Tensor], out: torch.Tensor | None = None) -> torch.Tensor:
+        if len(tensors) != len(self.shapes):
+            raise coatsim.ShapeMismatch("flatten: tensor count differs from the layout")
+        dev = tensors[0].device if tensors else None
+        if out is None:
+            out = torch.zeros(self.total, dtype=torch.float32, device=dev)
+        else:
+            out.zero_()
+        for t, s, o, n in zip(tensors, self.shapes, self.offsets, self.numels):
+            if tuple(t.shape) != s:
+                raise coatsim.ShapeMismatch("flatten: shape differs from the layout")
+            out[o:o + n].copy_(t.reshape(-1))
+        return out
+
+    def views(self, flat: torch.Tensor) -> list[torch.Tensor]:
+        return [flat[o:o + n].view(s) for s, o, n in zip(self.shapes, self.offsets, self.numels)]
+
+
+def _world(group) -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+def reduce_scatter_grads(g_full: torch.Tensor, g_shard: torch.Tensor, group=None, grad_op: str = "sum") -> None:
+    """g_shard = (sum over ranks of g_full)[this rank's shard]; grad_op="avg" divides by world size."""
+    ws, _ = _world(group)
+    if ws == 1:
+        if g_shard.data_ptr() != g_full.data_ptr():
+            g_shard.copy_(g_full[:g_shard.numel()])
+    else:
+        dist.reduce_scatter_tensor(g_shard, g_full, op=dist.ReduceOp.SUM, group=group)
+    if grad_op == "avg" and ws > 1:
+        g_shard.div_(ws)
+    elif grad_op not in ("sum", "avg"):
+        raise coatsim.InvalidSpec(f"grad_op must be 'sum' or 'avg', not {grad_op!r}")
+
+
+def all_gather_params(w_full: torch.Tensor, w_shard: torch.Tensor, group=None) -> None:
+    """Every rank's shard -> w_full on every rank (rank r's shard lands at
+    [r * n_shard, (r + 1) * n_shard)).  w_shard may alias its slot in w_full."""
+    ws, rank = _world(group)
+    if ws > 1:
+        dist.all_gather_into_tensor(w_full, w_shard, group=group)
+    else:
+        n = w_shard.numel()
+        if w_shard.data_ptr() != w_full.data_ptr():
+            w_full[:n].copy_(w_shard)
+
+
+def _all_flags(flags: torch.Tensor, group) -> int:
+    """OR of the device error words of all ranks (as 5 one-bit lanes, MAX-reduced)."""
+    ws, _ = _world(group)
+    if ws == 1:
+        return int(flags.item())
+    bits = torch.stack([(flags >> i) & 1 for i in range(5)]).reshape(-1).to(torch.int32)
+    dist.all_reduce(bits, op=dist.ReduceOp.MAX, group=group)
+    v = 0
+    for i, b in enumerate(bits.tolist()):
+        v |= (int(b) & 1) << i
+    return v
+
+
+class ZeroAdamW:
+    """FP8-DRE AdamW with the optimizer state partitioned over the ranks of
+    ``group`` (ZeRO stage 1/2): this rank owns parameters [lo, hi) of the flat
+    layout and only their E4M3 + DRE state."""
+
+    def __init__(self, shapes: Sequence[Sequence[int]], cfg: coatsim.AdamWConfig | None = None, group=None,
+                 device=None, grad_op: str = "sum"):
+        self.group = group
+        self.world_size, self.rank = _world(group)
+        self.layout = FlatLayout.build(shapes, self.world_size)
+        self.lo, self.hi = self.layout.shard(self.rank)
+        self.cfg = cfg or coatsim.AdamWConfig()
+        self.grad_op = grad_op
+        device = torch.device(device or "cuda")
+        self.slot = coatsim.make_slot([self.hi - self.lo], device=device)
+        self.g_shard = torch.empty(self.hi - self.lo, dtype=torch.float32, device=device)
+
+    @property
+    def step_count(self) -> int:
+        return self.slot.step
+
+    def step(self, w_full: torch.Tensor, g_full: torch.Tensor) -> None:
+        """One optimizer step on flat buffers of ``layout.total`` fp32 elements.
+        w_full is updated in place on every rank; raises the reference's
+        exception (the same one on every rank) on non-finite values."""
+        n = self.layout.total
+        if w_full.numel() != n or g_full.numel() != n:
+            raise coatsim.ShapeMismatch("ZeroAdamW.step: buffers do not match the flat layout")
+        if not w_full.is_contiguous() or not g_full.is_contiguous():
+            raise coatsim.InvalidSpec("ZeroAdamW.step: buffers must be contiguous")
+        reduce_scatter_grads(g_full, self.g_shard, self.group, self.grad_op)
+        coatsim._step_launch(w_full[self.lo:self.hi], self.g_shard, self.slot, self.cfg)
+        flags = _all_flags(self.slot._flags.t, self.group)
+        weights_change = not (flags & (_lib.FLAG_NONFINITE_GRAD | _lib.FLAG_CONTRACT))
+        try:
+            coatsim._step_commit(None, self.slot, flags)
+        finally:
+            if weights_change:
+                all_gather_params(w_full, self.slot._w_scratch, self.group)
