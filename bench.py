@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--mgaq-impl", default="graph", choices=["batch", "graph"],
+                    help="batch: coat_quantize_batch (one cooperative launch per layer); graph: the 9 "
+                         "per-tensor entry points replayed as a CUDA graph")
     ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "mgaq", "linear"],
                     help="adamw7b: BASELINE.json cfg3 (the headline); mgaq: cfg2 activation quantizers")
     return ap.parse_args()
@@ -427,42 +430,66 @@ def run_mgaq(args):
 
     def step(record=None):
         launches = 0
+        s = torch.cuda.current_stream()
         for name, r, c, G, x, codes, scales in bufs:
             if record is not None:
-                record[name][0].record(stream)
+                record[name][0].record(s)
             if G:
                 st = L.coat_quantize_per_group(x.data_ptr(), 1, r, c, G, codes.data_ptr(), scales.data_ptr(),
-                                               flags.data_ptr(), stream.cuda_stream)
+                                               flags.data_ptr(), s.cuda_stream)
                 launches += 1
             else:
-                st = L.coat_group_scale_max(x.data_ptr(), 1, r, c, 128, None, amax.data_ptr(), stream.cuda_stream)
+                st = L.coat_group_scale_max(x.data_ptr(), 1, r, c, 128, None, amax.data_ptr(), s.cuda_stream)
                 st = st or L.coat_quantize_per_tensor(x.data_ptr(), 1, r * c, amax.data_ptr(), codes.data_ptr(),
-                                                      scales.data_ptr(), flags.data_ptr(), stream.cuda_stream)
+                                                      scales.data_ptr(), flags.data_ptr(), s.cuda_stream)
                 launches += 3   # memset + amax + quant
             if record is not None:
-                record[name][1].record(stream)
+                record[name][1].record(s)
             assert st == 0, L.coat_last_error()
         return launches
 
+    items = (_lib.MgaqItemC * len(bufs))()
+    for i, (name, r, c, G, x, codes, scales) in enumerate(bufs):
+        items[i] = _lib.MgaqItemC(x.data_ptr(), 1, 0, r, c, G, codes.data_ptr(), scales.data_ptr(), None)
+
+    def batch_step():
+        st = L.coat_quantize_batch(items, len(bufs), flags.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert st == 0, L.coat_last_error()
+        return 2   # memset of the grid-barrier word + the cooperative kernel
+
     for _ in range(args.warmup):
         step()
+        batch_step()
     torch.cuda.synchronize()
+    if args.mgaq_impl == "graph":
+        # the layer's 9 quantizations replayed as one CUDA graph (no CPU launch gaps)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            step()   # warm the capture stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=side):
+                launches_per_step = step()
+        torch.cuda.synchronize()
+        run_once = graph.replay
+    else:
+        launches_per_step = 2
+        run_once = batch_step
     evs = {name: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for name, *_ in MGAQ_TENSORS}
     per = {name: 0.0 for name, *_ in MGAQ_TENSORS}
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(0)
-    launches = 0
     with sampler:
         start.record(stream)
         for _ in range(args.steps):
-            launches += step(evs)
-            for name in per:   # events are reused: accumulate after each step
-                pass
+            run_once()
         end.record(stream)
         torch.cuda.synchronize()
     ms = start.elapsed_time(end) / args.steps
-    # per-tensor timing from one extra instrumented pass
+    launches = launches_per_step * args.steps
+    # per-tensor timing from one extra instrumented (eager) pass
     step(evs)
     torch.cuda.synchronize()
     for name, *_ in MGAQ_TENSORS:
@@ -475,6 +502,8 @@ def run_mgaq(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
         "config": {"workload": "cfg2: MGAQ of one Llama-2-7B decoder layer, B4 x S2048 x H4096, I=11008",
+                   "impl": "coat_quantize_batch (1 cooperative launch)" if args.mgaq_impl == "batch"
+                           else "9 entry points as one CUDA graph",
                    "tensors": [t[:4] for t in MGAQ_TENSORS], "elements": nel,
                    "l2": "per-tensor inputs of 64-180 MB: stage-2 re-read partly L2-resident"},
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,

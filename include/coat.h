@@ -108,6 +108,29 @@ coat_status coat_quantize_per_tensor(const void* x, int dtype, int64_t n,
 coat_status coat_dequantize_per_tensor(const uint8_t* codes, const uint16_t* d_scale, int64_t n,
                                        void* out, int out_dtype, void* stream);
 
+/* ------------------------------------------------- batched MGAQ (layer) -- */
+/* Quantize a set of saved activations in ONE launch (the MGAQ call sites of a
+ * decoder layer, flow.cpp:450-480).  Per item, identical results to:
+ *   group_size > 0: coat_quantize_per_group(x, dtype, rows, cols, group_size)
+ *   group_size = 0: coat_group_scale_max(x, 128) + coat_quantize_per_tensor
+ *                   (scales -> the one BF16 scale; d_amax_bits, if non-NULL,
+ *                   receives the fp32 absmax bits)
+ * Requires rows*cols % 16 == 0, x 32-byte and codes 16-byte aligned, G/16 a
+ * power of two <= 32; at most 16 items.  d_flags ORs the non-finite flag of
+ * every item (COAT_ERR_NONFINITE_INPUT via coat_flags_to_status). */
+typedef struct coat_mgaq_item {
+    const void* x;
+    int32_t dtype;              /* 0 fp32, 1 bf16 */
+    int32_t reserved;
+    int64_t rows, cols;
+    int64_t group_size;         /* > 0 per-group, 0 per-tensor (Group Scaling amax) */
+    uint8_t* codes;
+    uint16_t* scales;
+    uint32_t* d_amax_bits;
+} coat_mgaq_item;
+coat_status coat_quantize_batch(const coat_mgaq_item* items, int32_t n_items, uint32_t* d_flags,
+                                void* stream);
+
 /* ------------------------------------------------------ range expansion -- */
 /* expand_quantize(x, G=128, e4m3) on a flat tensor (expand.hpp:67-68);
  * GeometryMismatch unless n % G == 0; InvalidSpec for G != 128. */

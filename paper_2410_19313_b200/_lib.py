@@ -47,6 +47,13 @@ class AdamWConfigC(C.Structure):
                 ("weight_decay", C.c_float), ("eps", C.c_float)]
 
 
+class MgaqItemC(C.Structure):
+    """coat_mgaq_item (include/coat.h)."""
+    _fields_ = [("x", C.c_void_p), ("dtype", C.c_int32), ("reserved", C.c_int32), ("rows", C.c_int64),
+                ("cols", C.c_int64), ("group_size", C.c_int64), ("codes", C.c_void_p), ("scales", C.c_void_p),
+                ("d_amax_bits", C.c_void_p)]
+
+
 _vp, _i64, _int, _u32p = C.c_void_p, C.c_int64, C.c_int, C.c_void_p
 
 _SIGS = {
@@ -62,6 +69,7 @@ _SIGS = {
     "coat_group_scale_max": ([_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp], _int),
     "coat_quantize_per_tensor": ([_vp, _int, _i64, _vp, _vp, _vp, _vp, _vp], _int),
     "coat_dequantize_per_tensor": ([_vp, _vp, _i64, _vp, _int, _vp], _int),
+    "coat_quantize_batch": ([C.POINTER(MgaqItemC), C.c_int32, _vp, _vp], _int),
     "coat_expand_quantize": ([_vp, _i64, _i64, MomentState, _vp, _vp], _int),
     "coat_dequantize_contract": ([MomentState, _i64, _i64, _vp, _vp, _vp], _int),
     "coat_make_slot": ([_i64, _i64, MomentState, MomentState, _vp], _int),

@@ -269,6 +269,41 @@ def quantize(x: torch.Tensor, geometry: QuantGeometry, format: Fp8Format | None 
     return QuantizedTensor(codes, scales, geometry, Fp8Tag.E4M3, tuple(x.shape))
 
 
+def quantize_batch(items: Sequence[tuple[torch.Tensor, QuantGeometry]]) -> list[QuantizedTensor]:
+    """MGAQ of a layer in one launch (coat_quantize_batch): the same results as
+    ``[quantize(x, g) for x, g in items]`` (per-group or per-tensor with Group
+    Scaling amax).  Up to 16 items; inputs 32-byte aligned with numel % 16 == 0."""
+    if not items:
+        return []
+    if len(items) > 16:
+        raise InvalidSpec("quantize_batch: at most 16 items")
+    arr = (_lib.MgaqItemC * len(items))()
+    out, keep = [], []
+    dev = None
+    for i, (x, geo) in enumerate(items):
+        x, dt = _as_device_input(x, "quantize_batch")
+        dev = x.device
+        rows, cols = _rows_cols(x.shape)
+        codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+        if geo.mode == QuantMode.PerGroup:
+            G = geo.group_size
+            if G <= 0 or cols % G != 0:
+                raise GeometryMismatch("per-group: last dim not divisible by group size")
+            scales = torch.empty(x.numel() // G, dtype=torch.bfloat16, device=x.device)
+        elif geo.mode == QuantMode.PerTensor:
+            G = 0
+            scales = torch.empty(1, dtype=torch.bfloat16, device=x.device)
+        else:
+            raise InvalidSpec("per-block geometry is outside the B200 hot path (SURVEY.md 2)")
+        arr[i] = _lib.MgaqItemC(x.data_ptr(), dt, 0, rows, cols, G, codes.data_ptr(), scales.data_ptr(), None)
+        keep.append(x)
+        out.append(QuantizedTensor(codes, scales, geo, Fp8Tag.E4M3, tuple(x.shape)))
+    fl = _Flags(dev)
+    _check(L.coat_quantize_batch(arr, len(items), fl.ptr, _stream()))
+    fl.raise_if_set("quantize")
+    return out
+
+
 def dequantize(q: QuantizedTensor, out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
     """quantize.hpp:72 (fp32 like the reference; bf16 optional)."""
     odt = 0 if out_dtype == torch.float32 else 1

@@ -21,103 +21,13 @@
 
 #include "coat_device.cuh"
 #include "coat_internal.h"
+#include "act_quant.cuh"
 
 namespace coat {
 namespace {
 
+using namespace aq;
 constexpr int kThreads = 256;
-
-struct Chunk16 {
-    float v[16];
-};
-
-template <int DT>  // 0: fp32, 1: bf16
-__device__ __forceinline__ Chunk16 load16(const void* x, int64_t e0) {
-    Chunk16 c;
-    if (DT == 0) {
-        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(x) + e0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float4 a = p[k];
-            c.v[4 * k] = a.x; c.v[4 * k + 1] = a.y; c.v[4 * k + 2] = a.z; c.v[4 * k + 3] = a.w;
-        }
-    } else {
-        const uint4* p = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + e0);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const uint4 a = p[k];
-            const uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                c.v[8 * k + 2 * i] = u2f(w[i] << 16);
-                c.v[8 * k + 2 * i + 1] = u2f(w[i] & 0xFFFF0000u);
-            }
-        }
-    }
-    return c;
-}
-
-template <int DT>
-__device__ __forceinline__ float load1(const void* x, int64_t i) {
-    if (DT == 0) return static_cast<const float*>(x)[i];
-    return u2f(uint32_t(static_cast<const uint16_t*>(x)[i]) << 16);
-}
-
-// |x| bit pattern for a max that ignores NaN like std::max(m, fabs(NaN)) == m
-// (quantize.cpp:104-105 / 137-139); Inf is kept.
-__device__ __forceinline__ uint32_t abs_bits_nan0(float x) {
-    const uint32_t a = f2u(x) & 0x7FFFFFFFu;
-    return a > 0x7F800000u ? 0u : a;
-}
-
-// RN(x / s) from rs = RN(1/s) (Markstein): exact for the quotient range that
-// matters to E4M3 (see header).
-__device__ __forceinline__ float quot_exact(float x, float s, float rs) {
-    const float q0 = __fmul_rn(x, rs);
-    return __fmaf_rn(__fmaf_rn(-q0, s, x), rs, q0);
-}
-
-__device__ __forceinline__ uint32_t encode_exact(float x, float s, float rs) {
-    return e4m3_encode(s >= 0x1p-100f ? quot_exact(x, s, rs) : __fdiv_rn(x, s));
-}
-
-// 16 codes from 16 values: paired Markstein quotients + one cvt per 2 values.
-__device__ __forceinline__ uint4 encode16(const Chunk16& c, float s, float rs, float nz) {
-    uint32_t w[4];
-    if (!(s >= 0x1p-100f)) {
-        // all-subnormal group: s = bf16_min_positive and 1/s overflows -- IEEE division
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            w[k] = 0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) w[k] |= e4m3_encode(__fdiv_rn(c.v[4 * k + i], s)) << (8 * i);
-        }
-        return make_uint4(w[0], w[1], w[2], w[3]);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        uint32_t h[2];
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            const F2 x{c.v[4 * k + 2 * p], c.v[4 * k + 2 * p + 1]};
-            const F2 q0 = f2_mul(x, f2s(rs), nz);
-            const F2 q = f2_fma(f2_fma(q0, f2s(-s), x), f2s(rs), q0);
-            h[p] = cvt_e4m3x2(q.x, q.y);
-        }
-        w[k] = h[0] | (h[1] << 16);
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-// Exact absmax bits of 16 values and a non-finite flag (bf16 pairs use 16-bit SIMD max).
-template <int DT>
-__device__ __forceinline__ uint32_t absmax16(const Chunk16& c, uint32_t& bad) {
-    uint32_t am = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) am = max(am, f2u(c.v[i]) & 0x7FFFFFFFu);
-    bad |= am >= 0x7F800000u;   // the max is >= every element, so any Inf/NaN shows here
-    return am;
-}
 
 // ---------------------------------------------------------------- per-group --
 // G = 16 * L with L in {1,2,4,8,16,32}: L lanes per group.
@@ -130,14 +40,19 @@ quant_group_kernel(const void* __restrict__ x, int64_t nchunks, uint8_t* __restr
     for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch - threadIdx.x % 32 < nchunks; ch += stride) {
         // keep whole warps in the loop so the group shuffles stay converged
         const bool valid = ch < nchunks;
-        Chunk16 c;
-        if (valid) c = load16<DT>(x, ch * 16);
-        uint32_t am = valid ? absmax16<DT>(c, bad) : 0u;
+        RawChunk<DT> raw;
+        uint32_t am = 0;
+        if (valid) {
+            raw = load_raw16<DT, EV_FIRST>(x, ch * 16);
+            am = absmax_raw<DT, false>(raw);
+        }
 #pragma unroll
         for (int off = 1; off < L; off <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
         if (valid) {
-            const float s = group_scale(u2f(am));
-            reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, __frcp_rn(s), nz);
+            bad |= am >= 0x7F800000u;   // the max is >= every element, so any Inf/NaN shows here
+            float s, rs;
+            group_scale_fast(am, s, rs);
+            reinterpret_cast<uint4*>(codes)[ch] = encode16(widen16<DT>(raw), s, rs, nz);
             if ((threadIdx.x % L) == 0) scales[ch / L] = float_to_bf16_bits_exact(s);
         }
     }
@@ -233,11 +148,7 @@ group_amax_kernel(const void* __restrict__ x, int64_t nchunks, float* __restrict
          ch += int64_t(gridDim.x) * kThreads) {
         const bool valid = ch < nchunks;
         uint32_t am = 0;
-        if (valid) {
-            const Chunk16 c = load16<DT>(x, ch * 16);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) am = max(am, abs_bits_nan0(c.v[i]));
-        }
+        if (valid) am = absmax_raw<DT, true>(load_raw16<DT, EV_LAST>(x, ch * 16));
 #pragma unroll
         for (int off = 1; off < L; off <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
         if (valid && inter && (threadIdx.x % L) == 0) inter[ch / L] = u2f(am);
@@ -271,7 +182,7 @@ group_amax_generic_kernel(const void* __restrict__ x, int64_t n, int64_t G, floa
 }
 
 // --------------------------------------------------------- per-tensor (K3) ----
-template <int DT>
+template <int DT, bool A32>
 __global__ void __launch_bounds__(kThreads)
 quant_tensor_kernel(const void* __restrict__ x, int64_t n, const uint32_t* amax_bits,
                     uint8_t* __restrict__ codes, uint16_t* scale_out, uint32_t* flags, float nz) {
@@ -282,9 +193,10 @@ quant_tensor_kernel(const void* __restrict__ x, int64_t n, const uint32_t* amax_
     const int64_t nchunks = n / 16;
     for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch < nchunks;
          ch += int64_t(gridDim.x) * kThreads) {
-        const Chunk16 c = load16<DT>(x, ch * 16);
-        absmax16<DT>(c, bad);
-        reinterpret_cast<uint4*>(codes)[ch] = encode16(c, s, inv_s, nz);
+        // second (last) pass over x: the amax pass left it in L2 (evict_last)
+        const RawChunk<DT> raw = A32 ? load_raw16<DT, EV_FIRST>(x, ch * 16) : load_raw16_a16<DT>(x, ch * 16);
+        bad |= absmax_raw<DT, false>(raw) >= 0x7F800000u;
+        reinterpret_cast<uint4*>(codes)[ch] = encode16(widen16<DT>(raw), s, inv_s, nz);
     }
     const int64_t t = nchunks * 16 + blockIdx.x * int64_t(kThreads) + threadIdx.x;
     if (blockIdx.x == 0 && t < n) {
@@ -352,12 +264,13 @@ static bool pow2_lanes(int64_t G, int* L) {
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }   // 256-bit loads
 
 cudaError_t launch_quantize_per_group(const void* x, int dtype, int64_t n, int64_t G, uint8_t* codes,
                                       uint16_t* scales, uint32_t* flags, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     int L = 0;
-    if (pow2_lanes(G, &L) && aligned16(x) && aligned16(codes)) {
+    if (pow2_lanes(G, &L) && aligned32(x) && aligned16(codes)) {
         const int64_t nchunks = n / 16;
         if (dtype == 0) {
             COAT_GROUP_SWITCH(L, (quant_group_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, codes, scales, flags, -0.0f)));
@@ -389,7 +302,7 @@ cudaError_t launch_group_amax(const void* x, int dtype, int64_t n, int64_t G, fl
     cudaError_t e = cudaMemsetAsync(global_bits, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess || n <= 0) return e;
     int L = 0;
-    if (pow2_lanes(G, &L) && aligned16(x)) {
+    if (pow2_lanes(G, &L) && aligned32(x)) {
         const int64_t nchunks = n / 16;
         if (dtype == 0) {
             COAT_GROUP_SWITCH(L, (group_amax_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, inter, global_bits)));
@@ -409,8 +322,14 @@ cudaError_t launch_quantize_per_tensor(const void* x, int dtype, int64_t n, cons
     if (n <= 0) return cudaSuccess;
     if (!aligned16(x) || !aligned16(codes)) return cudaErrorMisalignedAddress;
     const int blocks = blocks_for(imax64(n / 16, 1));
-    if (dtype == 0) quant_tensor_kernel<0><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
-    else quant_tensor_kernel<1><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
+    const bool a32 = aligned32(x);
+    if (dtype == 0) {
+        if (a32) quant_tensor_kernel<0, true><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
+        else quant_tensor_kernel<0, false><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
+    } else {
+        if (a32) quant_tensor_kernel<1, true><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
+        else quant_tensor_kernel<1, false><<<blocks, kThreads, 0, st>>>(x, n, amax_bits, codes, scale_out, flags, -0.0f);
+    }
     return cudaGetLastError();
 }
 

@@ -147,6 +147,29 @@ coat_status coat_dequantize_per_tensor(const uint8_t* codes, const uint16_t* d_s
     return cuda_status(launch_dequantize_per_group(codes, d_scale, n, n, out, out_dtype, S(stream)));
 }
 
+coat_status coat_quantize_batch(const coat_mgaq_item* items, int32_t n_items, uint32_t* d_flags, void* stream) {
+    if (n_items <= 0) return COAT_OK;
+    if (!items || n_items > kMgaqMaxItems) return fail(COAT_ERR_INVALID, "quantize_batch: 1..16 items");
+    MgaqItem it[kMgaqMaxItems];
+    for (int i = 0; i < n_items; ++i) {
+        const coat_mgaq_item& m = items[i];
+        const int64_t G = m.group_size;
+        if (G < 0) return fail(COAT_ERR_INVALID, "quantize_batch: negative group size");
+        const coat_status st = check_group(m.rows, m.cols, G ? G : m.cols, m.dtype);
+        if (st != COAT_OK) return st;
+        const int64_t n = m.rows * m.cols;
+        if (G) {
+            const int64_t l = G / 16;
+            if (G % 16 || l > 32 || (l & (l - 1))) return fail(COAT_ERR_INVALID, "quantize_batch: G/16 must be a power of two <= 32");
+        }
+        if (n % 16 || (reinterpret_cast<uintptr_t>(m.x) & 31u) || (reinterpret_cast<uintptr_t>(m.codes) & 15u) ||
+            !m.codes || !m.scales)
+            return fail(COAT_ERR_INVALID, "quantize_batch: needs numel % 16 == 0, 32-byte aligned x, 16-byte aligned codes");
+        it[i] = MgaqItem{m.x, (int)m.dtype, n, G, m.codes, m.scales, m.d_amax_bits};
+    }
+    return cuda_status(launch_mgaq_batch(it, n_items, d_flags, S(stream)));
+}
+
 // ------------------------------------------------------------------ DRE -----
 static const double kLogTarget = std::log(229376.0);  // expand.cpp:52 log(target_range)
 

@@ -73,6 +73,19 @@ cudaError_t launch_linear_wgrad(const uint16_t* xd, const uint16_t* sx, const ui
                                 float* dw, cudaStream_t st);
 cudaError_t launch_decode_e4m3_bf16(const uint8_t* codes, uint16_t* out, int64_t n, cudaStream_t st);
 
+// batched MGAQ (mgaq_batch.cu): one cooperative launch for a layer's quantizations
+constexpr int kMgaqMaxItems = 16;
+struct MgaqItem {
+    const void* x;
+    int dtype;              // 0 fp32, 1 bf16
+    int64_t n;              // elements (multiple of 16, 32-byte aligned x)
+    int64_t group_size;     // > 0: per-group(G), G/16 a power of two <= 32; 0: per-tensor
+    uint8_t* codes;
+    uint16_t* scales;       // [n/G] or one BF16 scale
+    uint32_t* amax_out;     // per-tensor: fp32 absmax bits (may be NULL)
+};
+cudaError_t launch_mgaq_batch(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t stream);
+
 // activation quantizers (act_quant.cu)
 cudaError_t launch_encode_e4m3(const float* x, uint8_t* out, int64_t n, uint32_t* flags,
                                cudaStream_t stream);

@@ -161,3 +161,36 @@ def test_llama_layer_sizes_bit_exact_sampled(coat, port):
     assert host(qt.scales)[0] == s
     exp = port.encode_e4m3((xs / s).astype(np.float32)).reshape(xs.shape)
     assert np.array_equal(host(qt.codes[sample]), exp)
+
+
+def test_quantize_batch_matches_single_calls(coat):
+    """coat_quantize_batch (one cooperative launch for a layer's MGAQ) is
+    bit-identical to the per-tensor entry points, mixed geometries and dtypes."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(3)
+    specs = [((96, 256), torch.bfloat16, coat.QuantGeometry.per_group(16)),
+             ((64, 512), torch.bfloat16, coat.QuantGeometry.per_tensor()),
+             ((33, 128), torch.float32, coat.QuantGeometry.per_group(128)),
+             ((40, 384), torch.float32, coat.QuantGeometry.per_tensor()),
+             ((7, 4096), torch.bfloat16, coat.QuantGeometry.per_group(32)),
+             ((129, 1024), torch.bfloat16, coat.QuantGeometry.per_tensor())]
+    xs = []
+    for shape, dt, geo in specs:
+        x = torch.randn(shape, device="cuda", generator=g) * 3
+        x[::17] *= 300
+        x[1, :5] = 0
+        xs.append((x.to(dt), geo))
+    batch = coat.quantize_batch(xs)
+    for (x, geo), qb in zip(xs, batch):
+        q = coat.quantize(x, geo)
+        assert torch.equal(q.codes, qb.codes)
+        assert torch.equal(q.scales.view(torch.int16), qb.scales.view(torch.int16))
+
+
+def test_quantize_batch_nonfinite_raises(coat):
+    import torch
+    x = torch.randn(64, 256, device="cuda").to(torch.bfloat16)
+    y = torch.randn(64, 256, device="cuda").to(torch.bfloat16)
+    y[5, 7] = float("inf")
+    with pytest.raises(coat.NonFiniteInput):
+        coat.quantize_batch([(x, coat.QuantGeometry.per_group(16)), (y, coat.QuantGeometry.per_tensor())])
