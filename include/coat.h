@@ -140,6 +140,21 @@ coat_status coat_expand_quantize(const float* x, int64_t n, int64_t group_size,
 coat_status coat_dequantize_contract(coat_moment_state in, int64_t n, int64_t group_size,
                                      float* x, uint32_t* d_flags, void* stream);
 
+/* ------------------------------------------------------ slot checkpoint -- */
+/* save_slot / load_slot (optimizer.hpp:72-75, optimizer.cpp:196-252): the
+ * {E4M3, expand, G} slot of a tensor of the given shape, state resident on the
+ * device, in the reference's binary format (u32 JSON header length + header +
+ * two ExpandedQuantState records, tensor_io.cpp:96-175).  Files are
+ * byte-identical to the reference's for the same state; either side loads the
+ * other's.  load: ShapeMismatch when the shape differs, InvalidSpec for another
+ * policy, BadMagic / IoError for malformed files. */
+coat_status coat_save_slot(const char* path, const int64_t* shape, int32_t rank, int64_t group_size,
+                           coat_moment_state m, coat_moment_state v, const coat_adamw_config* cfg,
+                           int64_t step, void* stream);
+coat_status coat_load_slot(const char* path, const int64_t* shape, int32_t rank, int64_t group_size,
+                           coat_moment_state m, coat_moment_state v, coat_adamw_config* cfg_out,
+                           int64_t* step_out, void* stream);
+
 /* ------------------------------------------------------------ optimizer -- */
 /* make_slot(shape, {E4M3, expand, G} x2) (optimizer.hpp:54) for n params. */
 coat_status coat_make_slot(int64_t n, int64_t group_size, coat_moment_state m,

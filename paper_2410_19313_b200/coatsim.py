@@ -15,6 +15,7 @@ Mapped surface (reference declaration -> here):
   expand.hpp:21-71                  ExpandedQuantState, expand_quantize, dequantize_contract
   optimizer.hpp:13-62               AdamWConfig, MomentPolicy, SlotPolicy, OptimizerSlot,
                                     make_slot, step
+  optimizer.hpp:72-75               save_slot, load_slot (the reference's file format)
 Out of scope: E5M2/DE8 formats, per-block geometry, FP32 scale
 dtype, the flow simulator and the memory model -- they raise InvalidSpec.
 """
@@ -22,6 +23,8 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import json
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -561,6 +564,39 @@ def step(params: torch.Tensor, grads: torch.Tensor, slot: OptimizerSlot, cfg: Ad
     (see _step_commit for the error semantics)."""
     _step_launch(params, grads, slot, cfg)
     _step_commit(params, slot, slot._flags.value() if check else 0)
+
+
+# ------------------------------------------------------- slot checkpoints ----
+def save_slot(path: str, slot: OptimizerSlot, cfg: AdamWConfig) -> None:
+    """optimizer.hpp:74 (optimizer.cpp:196-252): the reference's binary slot
+    format, byte-identical to what coatsim::save_slot writes for the same state."""
+    shape = (C.c_int64 * len(slot.shape))(*slot.shape)
+    c = cfg.c_struct()
+    _check(L.coat_save_slot(os.fsencode(path), shape, len(slot.shape), DRE_GROUP,
+                            slot._m[slot._cm].c_struct(), slot._v[slot._cv].c_struct(), C.byref(c),
+                            slot.step, _stream()))
+
+
+def load_slot(path: str, device="cuda") -> tuple[OptimizerSlot, AdamWConfig]:
+    """optimizer.hpp:75: load a slot written by the reference (or save_slot);
+    InvalidSpec unless the policy is {E4M3, expand, 128} for both moments."""
+    try:
+        with open(path, "rb") as f:
+            n = int.from_bytes(f.read(4), "little")
+            header = json.loads(f.read(n))
+        shape = [int(d) for d in header["shape"]]
+    except (OSError, ValueError, KeyError) as e:
+        raise IoError(f"load_slot: cannot read header of {path}: {e}") from None
+    slot = OptimizerSlot(shape, SlotPolicy(), torch.device(device))
+    cs = (C.c_int64 * len(shape))(*shape)
+    cfg_c = _lib.AdamWConfigC()
+    step = C.c_int64(0)
+    _check(L.coat_load_slot(os.fsencode(path), cs, len(shape), DRE_GROUP, slot._m[slot._cm].c_struct(),
+                            slot._v[slot._cv].c_struct(), C.byref(cfg_c), C.byref(step), _stream()))
+    slot.step = int(step.value)
+    cfg = AdamWConfig(beta1=cfg_c.beta1, beta2=cfg_c.beta2, lr=cfg_c.lr, weight_decay=cfg_c.weight_decay,
+                      eps=cfg_c.eps, step=slot.step)
+    return slot, cfg
 
 
 # ------------------------------------------------------------ FP8 linear ----

@@ -170,6 +170,38 @@ coat_status coat_quantize_batch(const coat_mgaq_item* items, int32_t n_items, ui
     return cuda_status(launch_mgaq_batch(it, n_items, d_flags, S(stream)));
 }
 
+// ------------------------------------------------------- slot checkpoints ----
+static coat_status check_slot_args(const char* path, const int64_t* shape, int32_t rank, int64_t G,
+                                   const coat_moment_state& m, const coat_moment_state& v) {
+    if (!path || !shape || rank <= 0) return fail(COAT_ERR_INVALID, "slot io: path/shape required");
+    for (int i = 0; i < rank; ++i)
+        if (shape[i] <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (G != 128) return fail(COAT_ERR_INVALID, "slot io: the B200 optimizer uses G = 128");
+    if (!m.codes || !m.scales || !m.k || !m.c || !v.codes || !v.scales || !v.k || !v.c)
+        return fail(COAT_ERR_INVALID, "slot io: NULL state buffer");
+    return COAT_OK;
+}
+
+coat_status coat_save_slot(const char* path, const int64_t* shape, int32_t rank, int64_t G, coat_moment_state m,
+                           coat_moment_state v, const coat_adamw_config* cfg, int64_t step, void* stream) {
+    coat_status st = check_slot_args(path, shape, rank, G, m, v);
+    if (st != COAT_OK) return st;
+    if (!cfg) return fail(COAT_ERR_INVALID, "save_slot: cfg is NULL");
+    std::string err;
+    st = save_slot_impl(path, shape, rank, G, m, v, *cfg, step, S(stream), err);
+    return st == COAT_OK ? st : fail(st, err.c_str());
+}
+
+coat_status coat_load_slot(const char* path, const int64_t* shape, int32_t rank, int64_t G, coat_moment_state m,
+                           coat_moment_state v, coat_adamw_config* cfg_out, int64_t* step_out, void* stream) {
+    coat_status st = check_slot_args(path, shape, rank, G, m, v);
+    if (st != COAT_OK) return st;
+    if (!cfg_out || !step_out) return fail(COAT_ERR_INVALID, "load_slot: outputs are NULL");
+    std::string err;
+    st = load_slot_impl(path, shape, rank, G, m, v, cfg_out, step_out, S(stream), err);
+    return st == COAT_OK ? st : fail(st, err.c_str());
+}
+
 // ------------------------------------------------------------------ DRE -----
 static const double kLogTarget = std::log(229376.0);  // expand.cpp:52 log(target_range)
 

@@ -56,6 +56,7 @@ cudaError_t launch_make_slot(const MomentStateOut& st, int64_t npad, cudaStream_
 
 // host_pipeline.cu: host-resident w/g streamed through K1 (state in HBM)
 }  // namespace coat
+#include <string>
 #include "../../include/coat.h"
 namespace coat {
 cudaError_t host_pipelined_step(const float* w_host_in, float* w_host_out, const float* g_host, int64_t n,
@@ -63,6 +64,14 @@ cudaError_t host_pipelined_step(const float* w_host_in, float* w_host_out, const
                                 const coat_moment_state& m_out, const coat_moment_state& v_out,
                                 const AdamWScalars& a, uint32_t* flags, unsigned long long* fallbacks,
                                 int64_t chunk, cudaStream_t stream);
+
+// slot checkpoints (slot_io.cu)
+coat_status save_slot_impl(const char* path, const int64_t* shape, int rank, int64_t G, const coat_moment_state& m,
+                           const coat_moment_state& v, const coat_adamw_config& cfg, int64_t step,
+                           cudaStream_t s, std::string& err);
+coat_status load_slot_impl(const char* path, const int64_t* shape, int rank, int64_t G, const coat_moment_state& m,
+                           const coat_moment_state& v, coat_adamw_config* cfg, int64_t* step, cudaStream_t s,
+                           std::string& err);
 
 // tcgen05 GEMMs (gemm_tcgen05.cu)
 cudaError_t launch_fp8_linear_fwd(const uint8_t* xc, const uint16_t* sx, const uint8_t* wc, const uint16_t* sw, int M,
