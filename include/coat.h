@@ -131,6 +131,27 @@ typedef struct coat_mgaq_item {
 coat_status coat_quantize_batch(const coat_mgaq_item* items, int32_t n_items, uint32_t* d_flags,
                                 void* stream);
 
+/* ----------------------------------------- fused producers + MGAQ (a17) -- */
+/* The RMSNorm block of the COAT forward (flow.cpp:546-549 / 597-599):
+ * x [rows, h] (fp32 / bf16) -> x_codes, x_scales = quantize(x, per_group(16))
+ * (rmsnorm1.in) and y_codes, *d_y_scale = quantize(rmsnorm(DQ(...), w), per_tensor)
+ * (qkv.in).  rmsnorm = flow.cpp:56-71 with the row sum in the reference's
+ * sequential order: codes and scales are bit-identical to the reference's tape.
+ * y never touches HBM unless y_out (fp32, may be NULL) is given; d_rms [rows]
+ * and *d_amax_bits receive the row rms and y's absmax bits.  h % 16 == 0. */
+coat_status coat_rmsnorm_quant(const void* x, int32_t dtype, int64_t rows, int64_t h, const float* w, float eps,
+                               uint8_t* x_codes, uint16_t* x_scales, uint8_t* y_codes, uint16_t* d_y_scale,
+                               float* y_out, float* d_rms, uint32_t* d_amax_bits, uint32_t* d_flags, void* stream);
+/* The SiLU*mul block (flow.cpp:603-612): gate, up [rows, cols] ->
+ * silu.in = Q_g16(gate), mul.in.silu = Q_g16(silu(DQ(silu.in))), mul.in.up =
+ * Q_g16(up), down.in = Q_t(DQ(mul.in.silu) * DQ(mul.in.up)).  silu uses CUDA's
+ * expf (the reference: glibc's); every quantizer is exact given its input.
+ * p_out (fp32, may be NULL) receives the product.  cols % 16 == 0. */
+coat_status coat_silu_mul_quant(const void* gate, const void* up, int32_t dtype, int64_t rows, int64_t cols,
+                                uint8_t* g_codes, uint16_t* g_scales, uint8_t* s_codes, uint16_t* s_scales,
+                                uint8_t* u_codes, uint16_t* u_scales, uint8_t* p_codes, uint16_t* d_p_scale,
+                                float* p_out, uint32_t* d_amax_bits, uint32_t* d_flags, void* stream);
+
 /* ------------------------------------------------------ range expansion -- */
 /* expand_quantize(x, G=128, e4m3) on a flat tensor (expand.hpp:67-68);
  * GeometryMismatch unless n % G == 0; InvalidSpec for G != 128. */

@@ -370,3 +370,27 @@ void oracle_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t
             for (int64_t j = 0; j < n; ++j) out[i * n + j] += av * b[p * n + j];
         }
 }
+
+/* --------------------------------------------------------- producers ---- */
+/* flow.cpp:56-71 rmsnorm_forward: per row a sequential fp32 sum of squares,
+ * var /= h, rms = sqrtf(var + eps), out = x / rms * w (each op rounded). */
+void oracle_rmsnorm(const float* x, const float* w, int64_t rows, int64_t h, float eps, float* out) {
+    for (int64_t r = 0; r < rows; ++r) {
+        float var = 0.0f;
+        for (int64_t j = 0; j < h; ++j) {
+            const float v = x[r * h + j];
+            var += v * v;
+        }
+        var /= (float)h;
+        const float rms = sqrtf(var + eps);
+        for (int64_t j = 0; j < h; ++j) out[r * h + j] = x[r * h + j] / rms * w[j];
+    }
+}
+
+/* flow.cpp:97-100 sigmoid / silu: x * (1 / (1 + expf(-x))). */
+void oracle_silu(const float* x, int64_t n, float* out) {
+    for (int64_t i = 0; i < n; ++i) {
+        const float s = 1.0f / (1.0f + expf(-x[i]));
+        out[i] = x[i] * s;
+    }
+}

@@ -63,6 +63,10 @@ uint64_t oracle_splitmix64_at(uint64_t seed, uint64_t i); /* i-th output of Spli
 /* flow.cpp:21-33 */
 void oracle_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n, float* out);
 
+/* producers (flow.cpp:56-71, 97-100) */
+void oracle_rmsnorm(const float* x, const float* w, int64_t rows, int64_t h, float eps, float* out);
+void oracle_silu(const float* x, int64_t n, float* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,8 @@ class Oracle:
             self._optk = self._fn("optimal_k", [C.c_double, C.POINTER(C.c_float),
                                                 C.POINTER(C.c_int)], None)
             self._matmul = self._fn("matmul", [_f32p, _f32p, _i64, _i64, _i64, _f32p], None)
+            self._rmsnorm = self._fn("rmsnorm", [_f32p, _f32p, _i64, _i64, _f, _f32p], None)
+            self._silu = self._fn("silu", [_f32p, _i64, _f32p], None)
         else:
             self._quant = self._fn("quantize", [_f32p, _i64p, C.c_int, C.c_int, _i64, _u8p,
                                                 _f32p, C.POINTER(C.c_int64)])
@@ -120,6 +122,9 @@ class Oracle:
                                        + [_i64, _f, _f, _f, _f, _f])
             self._load_slot = self._fn("load_slot", [C.c_char_p, _i64, _i64] + state + state
                                        + [C.POINTER(C.c_int64), _f32p])
+            self._tape = self._fn("layer_tape", [_i64, _i64, _i64, _i64, _i64, C.c_uint64, _f32p, C.c_char_p,
+                                                 _u8p, _f32p, C.POINTER(C.c_int64), C.POINTER(C.c_int),
+                                                 _f32p, _f32p])
 
     # --------------------------------------------------------------- codec --
     def encode_e4m3(self, x):
@@ -265,6 +270,33 @@ class Oracle:
                              C.byref(step), cfg5))
         cfg = dict(zip(["beta1", "beta2", "lr", "weight_decay", "eps"], map(float, cfg5)))
         return m, v, int(step.value), cfg
+
+    # ----------------------------------------------------------- producers --
+    def rmsnorm(self, x, w, eps=1e-6):
+        """flow.cpp:56-71 on (rows, h) fp32."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty_like(x)
+        self._rmsnorm(x, np.ascontiguousarray(w, np.float32), x.shape[0], x.shape[1], eps, out)
+        return out
+
+    def silu(self, x):
+        """flow.cpp:97-100."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty_like(x)
+        self._silu(x.reshape(-1), x.size, out.reshape(-1))
+        return out
+
+    def layer_tape(self, x, name, H, I, heads, S, B, seed=7):
+        """(codes, scales, kind, rms1, rms2) of one record of the reference forward's tape."""
+        assert self.kind == "reference"
+        x = np.ascontiguousarray(x, np.float32)
+        n = B * S * (H if name in ("rmsnorm1.in", "qkv.in", "attn.out", "rmsnorm2.in", "upgate.in") else I)
+        codes = np.empty(max(n, B * S * max(H, I)), np.uint8)
+        scales = np.empty(codes.size, np.float32)
+        ns, kind = C.c_int64(0), C.c_int(0)
+        r1, r2 = np.empty(H, np.float32), np.empty(H, np.float32)
+        _chk(self._tape(H, I, heads, S, B, seed, x, name.encode(), codes, scales, C.byref(ns), C.byref(kind), r1, r2))
+        return codes[:n], scales[:ns.value], kind.value, r1, r2
 
     # ----------------------------------------------------------- synthetic --
     def generate(self, kind: int, shape, frac=0.01, scale=100.0, seed=0):

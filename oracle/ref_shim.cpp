@@ -27,6 +27,7 @@
 
 #include "coatsim/errors.hpp"
 #include "coatsim/expand.hpp"
+#include "coatsim/flow.hpp"
 #include "coatsim/fp8.hpp"
 #include "coatsim/optimizer.hpp"
 #include "coatsim/quantize.hpp"
@@ -402,6 +403,41 @@ int ref_load_slot(const char* path, int64_t n, int64_t G, uint8_t* mc, float* ms
         cfg5[2] = cfg.lr;
         cfg5[3] = cfg.weight_decay;
         cfg5[4] = cfg.eps;
+    });
+}
+
+
+// Run the reference COAT DecoderLayer forward (flow.cpp:546-612) on x and
+// return one saved record of its tape: codes, scales (float) and -- for the
+// rmsnorm weights the producers need -- rms1/rms2.  kind: 0 per-group,
+// 1 per-tensor, 2 dense.  Test infrastructure for the fused producers.
+int ref_layer_tape(int64_t H, int64_t I, int64_t heads, int64_t S, int64_t B, uint64_t seed, const float* x,
+                   const char* name, uint8_t* codes, float* scales, int64_t* n_scales, int* kind, float* rms1,
+                   float* rms2) {
+    return guarded([&] {
+        LayerSpec spec;
+        spec.hidden = H;
+        spec.intermediate = I;
+        spec.num_heads = heads;
+        spec.seq_len = S;
+        spec.batch = B;
+        spec.group_size = 16;
+        spec.policy = FlowPolicy::COAT;
+        DecoderLayer layer(spec, LayerWeights::random(spec, seed));
+        const int64_t n = B * S * H;
+        const Tensor xt = Tensor::from({B, S, H}, std::vector<float>(x, x + n));
+        const ForwardResult res = layer.forward(xt);
+        const SavedActivation& rec = res.tape.find(name);
+        *kind = rec.kind == SaveKind::Fp8PerGroup ? 0 : rec.kind == SaveKind::Fp8PerTensor ? 1 : 2;
+        if (*kind <= 1) {
+            std::copy(rec.q.codes.begin(), rec.q.codes.end(), codes);
+            std::copy(rec.q.scales.begin(), rec.q.scales.end(), scales);
+            *n_scales = int64_t(rec.q.scales.size());
+        } else {
+            *n_scales = 0;
+        }
+        std::copy(layer.weights().rms1.data.begin(), layer.weights().rms1.data.end(), rms1);
+        std::copy(layer.weights().rms2.data.begin(), layer.weights().rms2.data.end(), rms2);
     });
 }
 

@@ -566,6 +566,62 @@ def step(params: torch.Tensor, grads: torch.Tensor, slot: OptimizerSlot, cfg: Ad
     _step_commit(params, slot, slot._flags.value() if check else 0)
 
 
+# --------------------------------------------- fused producers + MGAQ (a17) ----
+def rmsnorm_quantize(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6, return_y: bool = False):
+    """The RMSNorm block of the COAT forward (flow.cpp:546-549): returns
+    (Q_g16(x), Q_t(rmsnorm(DQ(Q_g16(x)), w)), rms per row[, y]) -- the
+    rmsnorm1.in / qkv.in records, bit-identical to the reference's tape."""
+    x, dt = _as_device_input(x, "rmsnorm_quantize")
+    rows, h = _rows_cols(x.shape)
+    w = w.to(device=x.device, dtype=torch.float32).contiguous()
+    if w.numel() != h:
+        raise ShapeMismatch("rmsnorm_quantize: weight must have h elements")
+    dev = x.device
+    xc = torch.empty(x.shape, dtype=torch.uint8, device=dev)
+    xs = torch.empty(x.numel() // 16, dtype=torch.bfloat16, device=dev)
+    yc = torch.empty(x.shape, dtype=torch.uint8, device=dev)
+    ys = torch.empty(1, dtype=torch.bfloat16, device=dev)
+    rms = torch.empty(rows, dtype=torch.float32, device=dev)
+    amax = torch.empty(1, dtype=torch.int32, device=dev)
+    y = torch.empty(x.shape, dtype=torch.float32, device=dev) if return_y else None
+    fl = _Flags(dev)
+    _check(L.coat_rmsnorm_quant(x.data_ptr(), dt, rows, h, w.data_ptr(), eps, xc.data_ptr(), xs.data_ptr(),
+                                yc.data_ptr(), ys.data_ptr(), _ptr(y), rms.data_ptr(), amax.data_ptr(), fl.ptr,
+                                _stream()))
+    fl.raise_if_set("rmsnorm_quantize")
+    qx = QuantizedTensor(xc, xs, QuantGeometry.per_group(16), Fp8Tag.E4M3, tuple(x.shape))
+    qy = QuantizedTensor(yc, ys, QuantGeometry.per_tensor(), Fp8Tag.E4M3, tuple(x.shape))
+    return (qx, qy, rms, y) if return_y else (qx, qy, rms)
+
+
+def silu_mul_quantize(gate: torch.Tensor, up: torch.Tensor, return_prod: bool = False):
+    """The SiLU*mul block (flow.cpp:603-612): returns the silu.in, mul.in.silu,
+    mul.in.up (per-group 1x16) and down.in (per-tensor) records[, prod]."""
+    gate, dt = _as_device_input(gate, "silu_mul_quantize")
+    up, dt2 = _as_device_input(up, "silu_mul_quantize")
+    if up.shape != gate.shape or dt2 != dt:
+        raise ShapeMismatch("silu_mul_quantize: gate and up must match in shape and dtype")
+    rows, cols = _rows_cols(gate.shape)
+    dev = gate.device
+    mk = lambda: (torch.empty(gate.shape, dtype=torch.uint8, device=dev),
+                  torch.empty(gate.numel() // 16, dtype=torch.bfloat16, device=dev))
+    (gc, gs), (sc, ss), (uc, us) = mk(), mk(), mk()
+    pc = torch.empty(gate.shape, dtype=torch.uint8, device=dev)
+    ps = torch.empty(1, dtype=torch.bfloat16, device=dev)
+    amax = torch.empty(1, dtype=torch.int32, device=dev)
+    p = torch.empty(gate.shape, dtype=torch.float32, device=dev) if return_prod else None
+    fl = _Flags(dev)
+    _check(L.coat_silu_mul_quant(gate.data_ptr(), up.data_ptr(), dt, rows, cols, gc.data_ptr(), gs.data_ptr(),
+                                 sc.data_ptr(), ss.data_ptr(), uc.data_ptr(), us.data_ptr(), pc.data_ptr(),
+                                 ps.data_ptr(), _ptr(p), amax.data_ptr(), fl.ptr, _stream()))
+    fl.raise_if_set("silu_mul_quantize")
+    g16, shp = QuantGeometry.per_group(16), tuple(gate.shape)
+    out = (QuantizedTensor(gc, gs, g16, Fp8Tag.E4M3, shp), QuantizedTensor(sc, ss, g16, Fp8Tag.E4M3, shp),
+           QuantizedTensor(uc, us, g16, Fp8Tag.E4M3, shp),
+           QuantizedTensor(pc, ps, QuantGeometry.per_tensor(), Fp8Tag.E4M3, shp))
+    return out + (p,) if return_prod else out
+
+
 # ------------------------------------------------------- slot checkpoints ----
 def save_slot(path: str, slot: OptimizerSlot, cfg: AdamWConfig) -> None:
     """optimizer.hpp:74 (optimizer.cpp:196-252): the reference's binary slot

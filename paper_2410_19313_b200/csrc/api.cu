@@ -170,6 +170,39 @@ coat_status coat_quantize_batch(const coat_mgaq_item* items, int32_t n_items, ui
     return cuda_status(launch_mgaq_batch(it, n_items, d_flags, S(stream)));
 }
 
+// ------------------------------------------------------- fused producers -----
+static bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+coat_status coat_rmsnorm_quant(const void* x, int32_t dtype, int64_t rows, int64_t h, const float* w, float eps,
+                               uint8_t* x_codes, uint16_t* x_scales, uint8_t* y_codes, uint16_t* d_y_scale,
+                               float* y_out, float* d_rms, uint32_t* d_amax_bits, uint32_t* d_flags, void* stream) {
+    const coat_status st = check_group(rows, h, 16, dtype);
+    if (st != COAT_OK) return st;
+    if (!x || !w || !x_codes || !x_scales || !y_codes || !d_y_scale || !d_rms || !d_amax_bits)
+        return fail(COAT_ERR_INVALID, "rmsnorm_quant: NULL buffer");
+    if (!a16(x) || !a16(w) || !a16(x_codes) || !a16(y_codes) || (y_out && !a16(y_out)))
+        return fail(COAT_ERR_INVALID, "rmsnorm_quant: buffers must be 16-byte aligned");
+    RmsBlockArgs a{x, dtype, rows, h, w, eps, x_codes, x_scales, y_codes, d_y_scale, y_out, d_rms, d_amax_bits, d_flags};
+    return cuda_status(launch_rmsnorm_block(a, S(stream)));
+}
+
+coat_status coat_silu_mul_quant(const void* gate, const void* up, int32_t dtype, int64_t rows, int64_t cols,
+                                uint8_t* g_codes, uint16_t* g_scales, uint8_t* s_codes, uint16_t* s_scales,
+                                uint8_t* u_codes, uint16_t* u_scales, uint8_t* p_codes, uint16_t* d_p_scale,
+                                float* p_out, uint32_t* d_amax_bits, uint32_t* d_flags, void* stream) {
+    const coat_status st = check_group(rows, cols, 16, dtype);
+    if (st != COAT_OK) return st;
+    if (!gate || !up || !g_codes || !g_scales || !s_codes || !s_scales || !u_codes || !u_scales || !p_codes ||
+        !d_p_scale || !d_amax_bits)
+        return fail(COAT_ERR_INVALID, "silu_mul_quant: NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(gate) & 31u) || (reinterpret_cast<uintptr_t>(up) & 31u) || !a16(g_codes) ||
+        !a16(s_codes) || !a16(u_codes) || !a16(p_codes) || (p_out && !a16(p_out)))
+        return fail(COAT_ERR_INVALID, "silu_mul_quant: gate/up 32-byte, codes 16-byte aligned");
+    SiluBlockArgs a{gate, up, dtype, rows * cols, g_codes, g_scales, s_codes, s_scales, u_codes, u_scales,
+                    p_codes, d_p_scale, p_out, d_amax_bits, d_flags};
+    return cuda_status(launch_silu_mul_block(a, S(stream)));
+}
+
 // ------------------------------------------------------- slot checkpoints ----
 static coat_status check_slot_args(const char* path, const int64_t* shape, int32_t rank, int64_t G,
                                    const coat_moment_state& m, const coat_moment_state& v) {

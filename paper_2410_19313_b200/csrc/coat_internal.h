@@ -95,6 +95,42 @@ struct MgaqItem {
 };
 cudaError_t launch_mgaq_batch(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t stream);
 
+// fused producers (producers.cu)
+struct RmsBlockArgs {
+    const void* x;
+    int dtype;
+    int64_t rows, h;
+    const float* w;
+    float eps;
+    uint8_t* xcodes;
+    uint16_t* xscales;
+    uint8_t* ycodes;
+    uint16_t* yscale;
+    float* yout;        // may be NULL
+    float* rms;         // [rows]
+    uint32_t* amax_bits;
+    uint32_t* flags;
+};
+struct SiluBlockArgs {
+    const void* gate;
+    const void* up;
+    int dtype;
+    int64_t n;
+    uint8_t* gcodes;
+    uint16_t* gscales;
+    uint8_t* scodes;
+    uint16_t* sscales;
+    uint8_t* ucodes;
+    uint16_t* uscales;
+    uint8_t* pcodes;
+    uint16_t* pscale;
+    float* pout;        // may be NULL
+    uint32_t* amax_bits;
+    uint32_t* flags;
+};
+cudaError_t launch_rmsnorm_block(const RmsBlockArgs& a, cudaStream_t stream);
+cudaError_t launch_silu_mul_block(const SiluBlockArgs& a, cudaStream_t stream);
+
 // activation quantizers (act_quant.cu)
 cudaError_t launch_encode_e4m3(const float* x, uint8_t* out, int64_t n, uint32_t* flags,
                                cudaStream_t stream);

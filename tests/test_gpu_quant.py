@@ -194,3 +194,26 @@ def test_quantize_batch_nonfinite_raises(coat):
     y[5, 7] = float("inf")
     with pytest.raises(coat.NonFiniteInput):
         coat.quantize_batch([(x, coat.QuantGeometry.per_group(16)), (y, coat.QuantGeometry.per_tensor())])
+
+
+@pytest.mark.parametrize("geo_g", [16, 128, 0])
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_signed_zero_inputs_encode_like_reference(coat, port, geo_g, dtype):
+    """encode_byte(-0) = 0x80 (fp8.cpp:53-88): -0 inputs keep their sign bit
+    through the exact (Markstein) quotient."""
+    import torch
+    x = port.generate(1, (32, 256), 0.05, 10.0, 5)
+    x[3, :40] = -0.0
+    x[4, 7] = 0.0
+    x[5, :] = -0.0          # an all -0 group row
+    xt = torch.from_numpy(x).cuda()
+    if dtype == "bf16":
+        xt = xt.to(torch.bfloat16)
+        x = xt.float().cpu().numpy()
+    geo = coat.QuantGeometry.per_group(geo_g) if geo_g else coat.QuantGeometry.per_tensor()
+    q = coat.quantize(xt, geo)
+    codes, scales = port.quantize(x, geo_g)
+    assert np.array_equal(q.codes.cpu().numpy(), codes)
+    assert np.array_equal(q.scales.float().cpu().numpy(), scales)
+    qb = coat.quantize_batch([(xt, geo)])[0]
+    assert np.array_equal(qb.codes.cpu().numpy(), codes)

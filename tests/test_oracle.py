@@ -332,3 +332,43 @@ def test_multithreaded_reference_is_bitwise_equal(ref):
     for key in ("codes", "scales", "k", "c"):
         assert np.array_equal(res[0][1][key], res[1][1][key])
         assert np.array_equal(res[0][2][key], res[1][2][key])
+
+
+def test_producer_port_reproduces_reference_layer_tape(port, ref):
+    """The fused-producer restatement (rmsnorm / silu / mul + MGAQ quantizers)
+    reproduces, bit for bit, the records the reference's COAT DecoderLayer
+    forward saves (flow.cpp:546-612): qkv.in, upgate.in, mul.in.silu, down.in."""
+    H, I, heads, S, B = 64, 128, 4, 32, 2
+    N = B * S
+    x = port.generate(1, (N, H), 0.05, 20.0, 3)
+
+    def rec(name):
+        return ref.layer_tape(x, name, H, I, heads, S, B)
+
+    def dq(codes, scales, G, shape):
+        return port.dequantize(codes.reshape(shape), scales, G)
+
+    c_in, s_in, k, rms1, rms2 = rec("rmsnorm1.in")
+    assert k == 0
+    pc, ps = port.quantize(x, 16)
+    assert np.array_equal(pc.reshape(-1), c_in) and np.array_equal(ps, s_in)
+    n1 = port.rmsnorm(dq(c_in, s_in, 16, (N, H)), rms1)
+    c_q, s_q, k, _, _ = rec("qkv.in")
+    pc, ps = port.quantize(n1, 0)
+    assert k == 1 and np.array_equal(pc.reshape(-1), c_q) and np.array_equal(ps, s_q)
+    # MLP half from the saved rmsnorm2.in record
+    c_r2, s_r2, _, _, _ = rec("rmsnorm2.in")
+    n2 = port.rmsnorm(dq(c_r2, s_r2, 16, (N, H)), rms2)
+    c_u, s_u, _, _, _ = rec("upgate.in")
+    pc, ps = port.quantize(n2, 0)
+    assert np.array_equal(pc.reshape(-1), c_u) and np.array_equal(ps, s_u)
+    c_g, s_g, _, _, _ = rec("silu.in")
+    silu = port.silu(dq(c_g, s_g, 16, (N, I)))
+    c_ms, s_ms, _, _, _ = rec("mul.in.silu")
+    pc, ps = port.quantize(silu, 16)
+    assert np.array_equal(pc.reshape(-1), c_ms) and np.array_equal(ps, s_ms)
+    c_mu, s_mu, _, _, _ = rec("mul.in.up")
+    prod = dq(c_ms, s_ms, 16, (N, I)) * dq(c_mu, s_mu, 16, (N, I))
+    c_d, s_d, _, _, _ = rec("down.in")
+    pc, ps = port.quantize(prod.astype(np.float32), 0)
+    assert np.array_equal(pc.reshape(-1), c_d) and np.array_equal(ps, s_d)
