@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--mgaq-impl", default="graph", choices=["batch", "graph"],
                     help="batch: coat_quantize_batch (one cooperative launch per layer); graph: the 9 "
                          "per-tensor entry points replayed as a CUDA graph")
-    ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "mgaq", "linear"],
+    ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "mgaq", "mgaq-fused", "linear"],
                     help="adamw7b: BASELINE.json cfg3 (the headline); mgaq: cfg2 activation quantizers")
     return ap.parse_args()
 
@@ -192,6 +192,9 @@ def main():
         return
     if args.workload == "mgaq":
         run_mgaq(args)
+        return
+    if args.workload == "mgaq-fused":
+        run_mgaq_fused(args)
         return
     if args.workload == "linear":
         run_linear(args)
@@ -509,6 +512,112 @@ def run_mgaq(args):
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "traffic": None, "peak_kind": kind, "algorithmic_bytes": alg_bytes},
         "per_tensor_ms": per, "clocks": sampler.summary(), "gpu_launches": launches,
+    }
+    print(json.dumps(out))
+
+
+# ------------------------------------- cfg2 with the producers fused (a17) ----
+def run_mgaq_fused(args):
+    """cfg2's nine MGAQ records of a Llama-2-7B layer produced by the fused
+    producer blocks (flow.cpp:546-612): coat_rmsnorm_quant x2 (rmsnorm1.in +
+    qkv.in, rmsnorm2.in + upgate.in), coat_silu_mul_quant (silu.in,
+    mul.in.silu, mul.in.up, down.in) and attn.out (Group Scaling amax +
+    per-tensor quantize; its producer, attention, is out of scope).  The
+    normalized activations and the SiLU product never touch HBM.  Compulsory
+    bytes: the five bf16 inputs once + every code and scale written (the second
+    read of attn.out is not counted)."""
+    import torch
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device=dev).manual_seed(7)
+    N, H, I = 8192, 4096, 11008
+
+    def act(r, c):
+        x = (torch.randn(r, c, device=dev, generator=gen) * 2).to(torch.bfloat16)
+        x[::100] *= 50
+        return x
+
+    x, r1, attn, gate, up = act(N, H), act(N, H), act(N, H), act(N, I), act(N, I)
+    w1 = (1 + 0.1 * torch.randn(H, device=dev, generator=gen)).float()
+    w2 = (1 + 0.1 * torch.randn(H, device=dev, generator=gen)).float()
+    u8 = lambda r, c: torch.empty(r, c, dtype=torch.uint8, device=dev)
+    sc = lambda n: torch.empty(n, dtype=torch.int16, device=dev)
+    rms = torch.empty(N, device=dev)
+    rms2 = torch.empty(N, device=dev)
+    amax = torch.empty(4, dtype=torch.int32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    bufs = {"x": (u8(N, H), sc(N * H // 16)), "n1": (u8(N, H), sc(1)), "r1": (u8(N, H), sc(N * H // 16)),
+            "n2": (u8(N, H), sc(1)), "g": (u8(N, I), sc(N * I // 16)), "s": (u8(N, I), sc(N * I // 16)),
+            "u": (u8(N, I), sc(N * I // 16)), "p": (u8(N, I), sc(1)), "attn": (u8(N, H), sc(1))}
+    B = {k: (c.data_ptr(), s_.data_ptr()) for k, (c, s_) in bufs.items()}
+    a0, a1, a2, a3 = (amax.data_ptr() + 4 * i for i in range(4))
+
+    branches = [torch.cuda.Stream() for _ in range(4)]
+
+    def step():
+        # the four blocks are independent: run them as parallel graph branches,
+        # so the latency-bound per-row sums overlap the bandwidth-bound kernels
+        main = torch.cuda.current_stream()
+        for b in branches:
+            b.wait_stream(main)
+        st = [b.cuda_stream for b in branches]
+        rc = L.coat_rmsnorm_quant(x.data_ptr(), 1, N, H, w1.data_ptr(), 1e-6, *B["x"], *B["n1"], None,
+                                  rms.data_ptr(), a0, flags.data_ptr(), st[0])
+        rc = rc or L.coat_rmsnorm_quant(r1.data_ptr(), 1, N, H, w2.data_ptr(), 1e-6, *B["r1"], *B["n2"], None,
+                                        rms2.data_ptr(), a1, flags.data_ptr(), st[1])
+        rc = rc or L.coat_silu_mul_quant(gate.data_ptr(), up.data_ptr(), 1, N, I, *B["g"], *B["s"], *B["u"],
+                                         *B["p"], None, a2, flags.data_ptr(), st[2])
+        rc = rc or L.coat_group_scale_max(attn.data_ptr(), 1, N, H, 128, None, a3, st[3])
+        rc = rc or L.coat_quantize_per_tensor(attn.data_ptr(), 1, N * H, a3, *B["attn"], flags.data_ptr(), st[3])
+        assert rc == 0, L.coat_last_error()
+        for b in branches:
+            main.wait_stream(b)
+        return 2 * 4 + 3 + 3   # rmsnorm: 3 kernels + memset; silu: 2 + memset; attn: memset + 2
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        step()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=side):
+            per_step = step()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(0)
+    with sampler:
+        start.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / args.steps
+    assert int(flags.item()) == 0
+    elems = 5 * N * H + 4 * N * I                  # the nine records (same elements as cfg2)
+    inputs = 2 * (4 * N * H + 2 * N * I)           # x, r1, attn, gate, up (bf16) read once
+    codes = elems                                   # one byte per element of every record
+    scales = 2 * (2 * N * H + 3 * N * I) // 16 + 2 * 4
+    alg = inputs + codes + scales
+    peak, kind = measured_peaks()
+    gbs = alg / (ms * 1e-3) / 1e9
+    out = {
+        "metric": "MGAQ + fused producers, Llama-2-7B layer (cfg2 records): elements/s & HBM GB/s",
+        "value": elems / (ms * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
+        "config": {"workload": "cfg2 records via fused producers: rmsnorm_quant x2, silu_mul_quant, attn.out per-tensor",
+                   "tokens": N, "hidden": H, "intermediate": I,
+                   "impl": "CUDA graph, the 4 independent blocks as parallel branches"},
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                     "traffic": None, "peak_kind": kind, "algorithmic_bytes": alg,
+                     "basis": "bf16 inputs once + all codes and scales written"},
+        "clocks": sampler.summary(), "gpu_launches": per_step * args.steps,
     }
     print(json.dumps(out))
 
