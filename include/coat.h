@@ -152,6 +152,21 @@ coat_status coat_silu_mul_quant(const void* gate, const void* up, int32_t dtype,
                                 uint8_t* u_codes, uint16_t* u_scales, uint8_t* p_codes, uint16_t* d_p_scale,
                                 float* p_out, uint32_t* d_amax_bits, uint32_t* d_flags, void* stream);
 
+/* -------------------------------------------- backward-side MGAQ pieces -- */
+/* SavedActivation::used_values_transposed (flow.cpp:360-395): out [cols, rows]
+ * = decode(codes[r, c]) * scale, the per-group scales (group_size % 16 == 0;
+ * 0 = per-tensor, one scale) following the original row-major grouping;
+ * codes_t (may be NULL) receives the transposed codes.  out_dtype 0 fp32 /
+ * 1 bf16.  Exact. */
+coat_status coat_transpose_dequantize(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,
+                                      int64_t group_size, void* out, int32_t out_dtype, uint8_t* codes_t,
+                                      void* stream);
+/* requantize_cached (flow.cpp:487-495): out = decode(encode(x / s)) * s with
+ * the BF16 scale cached in the forward (*d_scale); codes (may be NULL)
+ * receives the E4M3 codes.  x and out 16-byte aligned. */
+coat_status coat_requantize_cached(const void* x, int32_t dtype, int64_t n, const uint16_t* d_scale, void* out,
+                                   int32_t out_dtype, uint8_t* codes, uint32_t* d_flags, void* stream);
+
 /* ------------------------------------------------------ range expansion -- */
 /* expand_quantize(x, G=128, e4m3) on a flat tensor (expand.hpp:67-68);
  * GeometryMismatch unless n % G == 0; InvalidSpec for G != 128. */

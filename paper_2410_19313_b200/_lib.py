@@ -73,6 +73,8 @@ _SIGS = {
     "coat_rmsnorm_quant": ([_vp, C.c_int32, _i64, _i64, _vp, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                             _vp], _int),
     "coat_silu_mul_quant": ([_vp, _vp, C.c_int32, _i64, _i64] + [_vp] * 12, _int),
+    "coat_transpose_dequantize": ([_vp, _vp, _i64, _i64, _i64, _vp, C.c_int32, _vp, _vp], _int),
+    "coat_requantize_cached": ([_vp, C.c_int32, _i64, _vp, _vp, C.c_int32, _vp, _vp, _vp], _int),
     "coat_save_slot": ([C.c_char_p, C.POINTER(C.c_int64), C.c_int32, _i64, MomentState, MomentState,
                         C.POINTER(AdamWConfigC), _i64, _vp], _int),
     "coat_load_slot": ([C.c_char_p, C.POINTER(C.c_int64), C.c_int32, _i64, MomentState, MomentState,

@@ -622,6 +622,60 @@ def silu_mul_quantize(gate: torch.Tensor, up: torch.Tensor, return_prod: bool = 
     return out + (p,) if return_prod else out
 
 
+# -------------------------------------------------- backward-side MGAQ pieces ----
+def used_values_transposed(q: QuantizedTensor, out_dtype: torch.dtype = torch.float32,
+                           return_codes: bool = False):
+    """SavedActivation::used_values_transposed (flow.cpp:360-395): the
+    dequantized transpose [cols, rows] of a 2-D FP8 save (wgrad operand);
+    per-group scales follow the original row-major grouping."""
+    if q.geometry.mode not in (QuantMode.PerGroup, QuantMode.PerTensor):
+        raise InvalidSpec("per-block geometry is outside the B200 hot path (SURVEY.md 2)")
+    rows, cols = _rows_cols(q.source_shape)
+    G = q.geometry.group_size if q.geometry.mode == QuantMode.PerGroup else 0
+    dev = q.codes.device
+    out = torch.empty(cols, rows, dtype=out_dtype, device=dev)
+    ct = torch.empty(cols, rows, dtype=torch.uint8, device=dev) if return_codes else None
+    _check(L.coat_transpose_dequantize(q.codes.data_ptr(), q.scales.data_ptr(), rows, cols, G, out.data_ptr(),
+                                       0 if out_dtype == torch.float32 else 1, _ptr(ct), _stream()))
+    return (out, ct) if return_codes else out
+
+
+def requantize_cached(x: torch.Tensor, cached_scale: torch.Tensor, out_dtype: torch.dtype = torch.float32,
+                      return_codes: bool = False):
+    """requantize_cached (flow.cpp:487-495): decode(encode(x / s)) * s against
+    the per-tensor BF16 scale cached in the forward (``cached_scale``, 1 element)."""
+    x, dt = _as_device_input(x, "requantize_cached")
+    s = cached_scale.to(device=x.device, dtype=torch.bfloat16).reshape(1).contiguous()
+    out = torch.empty(x.shape, dtype=out_dtype, device=x.device)
+    codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device) if return_codes else None
+    fl = _Flags(x.device)
+    _check(L.coat_requantize_cached(x.data_ptr(), dt, x.numel(), s.data_ptr(), out.data_ptr(),
+                                    0 if out_dtype == torch.float32 else 1, _ptr(codes), fl.ptr, _stream()))
+    fl.raise_if_set("requantize_cached")
+    return (out, codes) if return_codes else out
+
+
+class WeightOperandCache:
+    """DecoderLayer::weight_operand + start_accumulation_cycle (flow.cpp:499-530):
+    a master weight is quantized per-tensor (Group Scaling amax) at most once
+    per gradient-accumulation cycle; later uses in the cycle reuse the codes."""
+
+    def __init__(self):
+        self._cache: dict = {}
+        self.weight_scale_computations = 0
+
+    def start_accumulation_cycle(self) -> None:
+        self._cache.clear()
+
+    def operand(self, name: str, master: torch.Tensor) -> QuantizedTensor:
+        q = self._cache.get(name)
+        if q is None:
+            q = quantize(master, QuantGeometry.per_tensor())
+            self._cache[name] = q
+            self.weight_scale_computations += 1
+        return q
+
+
 # ------------------------------------------------------- slot checkpoints ----
 def save_slot(path: str, slot: OptimizerSlot, cfg: AdamWConfig) -> None:
     """optimizer.hpp:74 (optimizer.cpp:196-252): the reference's binary slot

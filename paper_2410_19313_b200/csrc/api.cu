@@ -203,6 +203,30 @@ coat_status coat_silu_mul_quant(const void* gate, const void* up, int32_t dtype,
     return cuda_status(launch_silu_mul_block(a, S(stream)));
 }
 
+// ------------------------------------------------- backward-side MGAQ pieces ----
+coat_status coat_transpose_dequantize(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,
+                                      int64_t G, void* out, int32_t out_dtype, uint8_t* codes_t, void* stream) {
+    if (rows <= 0 || cols <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if (out_dtype != 0 && out_dtype != 1) return fail(COAT_ERR_INVALID, "dtype must be 0 (fp32) or 1 (bf16)");
+    if (G < 0 || (G > 0 && (cols % G != 0)))
+        return fail(COAT_ERR_GEOMETRY, "per-group: last dim not divisible by group size");
+    if (G > 0 && G % 16 != 0) return fail(COAT_ERR_INVALID, "transpose_dequantize: group size must be a multiple of 16");
+    if (!codes || !scales || !out) return fail(COAT_ERR_INVALID, "transpose_dequantize: NULL buffer");
+    return cuda_status(launch_transpose_dequant(codes, scales, rows, cols, G, out, out_dtype, codes_t, S(stream)));
+}
+
+coat_status coat_requantize_cached(const void* x, int32_t dtype, int64_t n, const uint16_t* d_scale, void* out,
+                                   int32_t out_dtype, uint8_t* codes, uint32_t* d_flags, void* stream) {
+    if (n <= 0) return fail(COAT_ERR_INVALID, "tensor dimensions must be positive");
+    if ((dtype != 0 && dtype != 1) || (out_dtype != 0 && out_dtype != 1))
+        return fail(COAT_ERR_INVALID, "dtype must be 0 (fp32) or 1 (bf16)");
+    if (!x || !d_scale || !out) return fail(COAT_ERR_INVALID, "requantize_cached: NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) || (reinterpret_cast<uintptr_t>(out) & 15u) ||
+        (codes && (reinterpret_cast<uintptr_t>(codes) & 15u)))
+        return fail(COAT_ERR_INVALID, "requantize_cached: buffers must be 16-byte aligned");
+    return cuda_status(launch_requantize_cached(x, dtype, n, d_scale, out, out_dtype, codes, d_flags, S(stream)));
+}
+
 // ------------------------------------------------------- slot checkpoints ----
 static coat_status check_slot_args(const char* path, const int64_t* shape, int32_t rank, int64_t G,
                                    const coat_moment_state& m, const coat_moment_state& v) {

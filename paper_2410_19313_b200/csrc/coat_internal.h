@@ -131,6 +131,12 @@ struct SiluBlockArgs {
 cudaError_t launch_rmsnorm_block(const RmsBlockArgs& a, cudaStream_t stream);
 cudaError_t launch_silu_mul_block(const SiluBlockArgs& a, cudaStream_t stream);
 
+// backward-side MGAQ pieces (mgaq_bwd.cu)
+cudaError_t launch_transpose_dequant(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,
+                                     int64_t G, void* out, int out_dtype, uint8_t* codes_t, cudaStream_t stream);
+cudaError_t launch_requantize_cached(const void* x, int dtype, int64_t n, const uint16_t* scale, void* out,
+                                     int out_dtype, uint8_t* codes, uint32_t* flags, cudaStream_t stream);
+
 // activation quantizers (act_quant.cu)
 cudaError_t launch_encode_e4m3(const float* x, uint8_t* out, int64_t n, uint32_t* flags,
                                cudaStream_t stream);
