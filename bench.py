@@ -344,7 +344,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": sampler.summary(),
-            "gpu_launches": args.steps,
+            # K1 on the whole rounds + the generic kernel on the n % round tail (if any);
+            # round = 12 groups (COAT_K1_EW=8: 16) of 128 params (k1_ws.cu)
+            "gpu_launches": args.steps * (1 + (1 if n % (2048 if os.environ.get("COAT_K1_EW") == "8" else 1536)
+                                               else 0)),
         }
         print(json.dumps(out))
     if ws > 1:
