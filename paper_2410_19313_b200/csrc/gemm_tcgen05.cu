@@ -12,15 +12,26 @@
 //   A: M x K, K-major (memory [M][K]) or MN-major (memory [K][M])
 //   B: N x K, K-major (memory [N][K]) or MN-major (memory [K][N])
 //   kind::f8f6f4 (E4M3 x E4M3) or kind::f16 (BF16 x BF16), fp32 accumulate in TMEM.
-// Tile 128 x 256 x 128 bytes of K, 4-stage TMA (SWIZZLE_128B) -> smem ring,
-// persistent CTAs (one per SM), warp-specialized:
+// Persistent, warp-specialized, TMA (SWIZZLE_128B) -> smem ring of 128-byte K
+// slices:
 //   warp 0: TMA producer (one elected lane)       full/empty mbarriers per stage
 //   warp 1: TMEM allocator + MMA issuer (one lane) tcgen05.mma + tcgen05.commit
 //   warps 2-5: epilogue (TMEM lanes 0-127)        double-buffered accumulator
+// Two variants (kCta):
+//   1: one CTA per SM, 128 x 256 tile, cta_group::1 (small M).
+//   2: a CTA pair on the two SMs of a TPC (cluster of 2), 256 x 256 tile,
+//      tcgen05.mma.cta_group::2 issued by the leader.  Each CTA stages only its
+//      128 rows of A and its 128-column half of B (32 KB per stage instead of
+//      48 KB for half the FLOPs), so the L2->SM operand traffic per FLOP drops
+//      by a third -- the 1-CTA kernel is operand-bandwidth bound at ~70% of the
+//      tensor pipe.  Both CTAs' TMA bytes land on the leader's full barrier
+//      (.cta_group::2 TMA, mapa address); commits multicast to both CTAs; both
+//      CTAs' epilogues arrive on the leader's TMEM-empty barrier.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "coat_device.cuh"
@@ -29,17 +40,26 @@
 namespace coat {
 namespace gemm {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BM = 128;                   // accumulator rows per CTA (TMEM lanes)
+constexpr int BN = 256;                   // accumulator columns (MMA N)
 constexpr int BKB = 128;                  // K bytes per stage (one 128B swizzle row)
-constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BKB;         // 16 KiB
-constexpr int B_BYTES = BN * BKB;         // 32 KiB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 192;
 constexpr int ACC_COLS = BN;              // fp32 columns per accumulator
 constexpr int TMEM_COLS = 2 * ACC_COLS;   // double buffer = all 512 columns
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+template <int kCta>
+struct Geo {
+    static constexpr int BN_L = BN / kCta;                 // B rows staged by this CTA
+    static constexpr int B_BYTES = BN_L * BKB;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+#ifndef COAT_GEMM_PAIR_STAGES
+#define COAT_GEMM_PAIR_STAGES 6
+#endif
+    static constexpr int STAGES = kCta == 2 ? COAT_GEMM_PAIR_STAGES : 4;
+    static constexpr int TILE_M = BM * kCta;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 struct Params {
     int M, N, K;               // K in elements
@@ -80,21 +100,63 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of `p` (a local smem object) in cluster CTA `rank`
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+// TMA into this CTA's smem, completion bytes counted on the pair leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int x, int y, uint32_t bar_caddr) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(bar_caddr)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(uint16_t(3))
+        : "memory");
+}
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
-template <bool kF8>
+template <bool kF8, int kCta>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    if (kF8) {
+    if (kF8 && kCta == 1) {
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
             "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-    } else {
+    } else if (kCta == 1) {
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+    } else if (kF8) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
     }
 }
@@ -117,14 +179,17 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
 }
 
 // Instruction descriptor: fp32 accumulate, E4M3 (0) or BF16 (1) operands.
-__host__ __device__ constexpr uint32_t instr_desc(bool f8, bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t instr_desc(bool f8, bool a_mn, bool b_mn, int m) {
     return (1u << 4) | ((f8 ? 0u : 1u) << 7) | ((f8 ? 0u : 1u) << 10) | ((a_mn ? 1u : 0u) << 15) |
-           ((b_mn ? 1u : 0u) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+           ((b_mn ? 1u : 0u) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
-template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16>
+template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16, int kCta>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params P) {
+    using G = Geo<kCta>;
+    constexpr int STAGES = G::STAGES;
+    constexpr int STAGE_BYTES = G::STAGE_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -138,6 +203,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     constexpr int BK = BKB / ESZ;                  // K elements per stage
     constexpr int UK = 32 / ESZ;                   // K elements per MMA (32 bytes)
     const int ntiles = P.tiles_m * P.tiles_n;
+    const uint32_t rank = kCta == 2 ? cluster_rank() : 0u;
+    const int tile0 = blockIdx.x / kCta, tstep = gridDim.x / kCta;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -146,21 +213,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);          // one arrive per epilogue warp
+            mbar_init(&tempty[a], 4 * kCta);   // one arrive per epilogue warp of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (kCta == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        }
     }
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
     }
     tc_fence_before();
-    __syncthreads();
+    if (kCta == 2) cluster_sync_all();   // barriers initialised in both CTAs before any remote use
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -169,27 +245,49 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for (int tile = tile0; tile < ntiles; tile += tstep) {
                 const int mb = tile % P.tiles_m, nb = tile / P.tiles_m;
+                const int m0 = mb * G::TILE_M + int(rank) * BM;     // this CTA's A rows
+                const int n0 = nb * BN + int(rank) * G::BN_L;       // this CTA's B rows
                 for (int kb = 0; kb < P.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     uint8_t* sb = sa + A_BYTES;
-                    mbar_expect_tx(&full[stage], STAGE_BYTES);
                     const int k0 = kb * BK;
-                    if (!kAMN) {
-                        tma_load_2d(sa, &map_a, k0, mb * BM, &full[stage]);
-                    } else {
+                    if (kCta == 1) {
+                        mbar_expect_tx(&full[stage], STAGE_BYTES);
+                        if (!kAMN) {
+                            tma_load_2d(sa, &map_a, k0, m0, &full[stage]);
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < BM * ESZ / 128; ++c)
-                            tma_load_2d(sa + c * BK * 128, &map_a, mb * BM + c * (128 / ESZ), k0, &full[stage]);
-                    }
-                    if (!kBMN) {
-                        tma_load_2d(sb, &map_b, k0, nb * BN, &full[stage]);
-                    } else {
+                            for (int c = 0; c < BM * ESZ / 128; ++c)
+                                tma_load_2d(sa + c * BK * 128, &map_a, m0 + c * (128 / ESZ), k0, &full[stage]);
+                        }
+                        if (!kBMN) {
+                            tma_load_2d(sb, &map_b, k0, n0, &full[stage]);
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < BN * ESZ / 128; ++c)
-                            tma_load_2d(sb + c * BK * 128, &map_b, nb * BN + c * (128 / ESZ), k0, &full[stage]);
+                            for (int c = 0; c < G::BN_L * ESZ / 128; ++c)
+                                tma_load_2d(sb + c * BK * 128, &map_b, n0 + c * (128 / ESZ), k0, &full[stage]);
+                        }
+                    } else {
+                        // the leader's full barrier counts both CTAs' bytes
+                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                        const uint32_t fb = cluster_addr(&full[stage], 0);
+                        if (!kAMN) {
+                            tma_load_2d_pair(sa, &map_a, k0, m0, fb);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < BM * ESZ / 128; ++c)
+                                tma_load_2d_pair(sa + c * BK * 128, &map_a, m0 + c * (128 / ESZ), k0, fb);
+                        }
+                        if (!kBMN) {
+                            tma_load_2d_pair(sb, &map_b, k0, n0, fb);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < G::BN_L * ESZ / 128; ++c)
+                                tma_load_2d_pair(sb + c * BK * 128, &map_b, n0 + c * (128 / ESZ), k0, fb);
+                        }
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -199,9 +297,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = instr_desc(kF8, kAMN, kBMN);
+        // ------------------------------------------------------ MMA issuer (pair: leader only)
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = instr_desc(kF8, kAMN, kBMN, G::TILE_M);
             // per-MMA K advance inside a stage (bytes): K-major +32 B, MN-major +UK rows of 128 B
             constexpr uint32_t a_step = kAMN ? UK * 128 : 32;
             constexpr uint32_t b_step = kBMN ? UK * 128 : 32;
@@ -211,7 +309,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for (int tile = tile0; tile < ntiles; tile += tstep) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1u);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + uint32_t(acc * ACC_COLS);
@@ -224,15 +322,19 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                     for (int kk = 0; kk < BK / UK; ++kk) {
                         const uint64_t ad = smem_desc(sa + kk * a_step, a_lbo, 1024);
                         const uint64_t bd = smem_desc(sb + kk * b_step, b_lbo, 1024);
-                        tc_mma<kF8>(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        tc_mma<kF8, kCta>(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                     }
-                    tc_commit(&empty[stage]);      // frees the smem stage when these MMAs retire
+                    // frees the smem stage (in both CTAs) when these MMAs retire
+                    if (kCta == 1) tc_commit(&empty[stage]);
+                    else tc_commit_pair(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                tc_commit(&tfull[acc]);            // accumulator ready for the epilogue
+                // accumulator ready for the epilogue(s)
+                if (kCta == 1) tc_commit(&tfull[acc]);
+                else tc_commit_pair(&tfull[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1u;
@@ -242,17 +344,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     } else {
         // ------------------------------------------------------ epilogue (warps 2..5)
         const int q = warp & 3;                    // TMEM lane quarter this warp may access
-        const int row_in_tile = q * 32 + lane;
+        const int row_in_tile = int(rank) * BM + q * 32 + lane;
+        const uint32_t tempty_leader0 = kCta == 2 ? cluster_addr(&tempty[0], 0) : 0u;
         float alpha = P.alpha;
         if (P.scale_a) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_a));
         if (P.scale_b) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_b));
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int tile = tile0; tile < ntiles; tile += tstep) {
             const int mb = tile % P.tiles_m, nb = tile / P.tiles_m;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = mb * BM + row_in_tile;
+            const int row = mb * G::TILE_M + row_in_tile;
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * ACC_COLS);
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
@@ -296,7 +399,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (kCta == 1) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(tempty_leader0 + uint32_t(acc * sizeof(uint64_t)));
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1u;
@@ -304,10 +410,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (kCta == 2) cluster_sync_all();   // no CTA of the pair leaves while the other may still signal it
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        if (kCta == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
     }
 }
 
@@ -341,22 +451,24 @@ bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t c
     return r == CUDA_SUCCESS;
 }
 
-template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16>
-cudaError_t run(const void* a, const void* b, int M, int N, int K, float alpha, const uint16_t* sa,
-                const uint16_t* sb, void* out, int64_t ldo, cudaStream_t stream) {
+template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16, int kCta>
+cudaError_t run_cta(const void* a, const void* b, int M, int N, int K, float alpha, const uint16_t* sa,
+                    const uint16_t* sb, void* out, int64_t ldo, cudaStream_t stream) {
+    using G = Geo<kCta>;
     constexpr int ESZ = kF8 ? 1 : 2;
     constexpr int BK = BKB / ESZ;
     CUtensorMap ma, mb;
     // A logical [M x K]: K-major memory [M][K]; MN-major memory [K][M]
     const bool ok_a = !kAMN ? make_map(&ma, a, ESZ, M, K, BK, BM) : make_map(&ma, a, ESZ, K, M, 128 / ESZ, BK);
-    const bool ok_b = !kBMN ? make_map(&mb, b, ESZ, N, K, BK, BN) : make_map(&mb, b, ESZ, K, N, 128 / ESZ, BK);
+    const bool ok_b =
+        !kBMN ? make_map(&mb, b, ESZ, N, K, BK, G::BN_L) : make_map(&mb, b, ESZ, K, N, 128 / ESZ, BK);
     if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-    auto kern = gemm_kernel<kF8, kAMN, kBMN, kOutBf16>;
+    auto kern = gemm_kernel<kF8, kAMN, kBMN, kOutBf16, kCta>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (attr_dev != dev) {
-        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
@@ -364,7 +476,7 @@ cudaError_t run(const void* a, const void* b, int M, int N, int K, float alpha, 
     P.M = M;
     P.N = N;
     P.K = K;
-    P.tiles_m = (M + BM - 1) / BM;
+    P.tiles_m = (M + G::TILE_M - 1) / G::TILE_M;
     P.tiles_n = (N + BN - 1) / BN;
     P.k_blocks = (K + BK - 1) / BK;
     P.alpha = alpha;
@@ -373,9 +485,42 @@ cudaError_t run(const void* a, const void* b, int M, int N, int K, float alpha, 
     P.out = out;
     P.ldo = ldo;
     const int ntiles = P.tiles_m * P.tiles_n;
-    const int grid = ntiles < device_sm_count() ? ntiles : device_sm_count();
-    kern<<<grid, THREADS, SMEM_BYTES, stream>>>(ma, mb, P);
-    return cudaGetLastError();
+    const int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
+    const int grid = kCta * (ntiles < units ? ntiles : units);
+    if (kCta == 1) {
+        kern<<<grid, THREADS, G::SMEM_BYTES, stream>>>(ma, mb, P);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = G::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, ma, mb, P);
+}
+
+// COAT_GEMM_CTA=1 forces the single-CTA kernel (A/B comparisons).
+inline int pair_mode() {
+    static const int v = [] {
+        const char* e = getenv("COAT_GEMM_CTA");
+        return (e && e[0] == '1') ? 1 : 2;
+    }();
+    return v;
+}
+
+template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16>
+cudaError_t run(const void* a, const void* b, int M, int N, int K, float alpha, const uint16_t* sa,
+                const uint16_t* sb, void* out, int64_t ldo, cudaStream_t stream) {
+    if (M > BM && pair_mode() == 2)
+        return run_cta<kF8, kAMN, kBMN, kOutBf16, 2>(a, b, M, N, K, alpha, sa, sb, out, ldo, stream);
+    return run_cta<kF8, kAMN, kBMN, kOutBf16, 1>(a, b, M, N, K, alpha, sa, sb, out, ldo, stream);
 }
 
 }  // namespace gemm
