@@ -60,6 +60,8 @@ _SIGS = {
     "coat_version": ([], C.c_char_p),
     "coat_status_string": ([_int], C.c_char_p),
     "coat_last_error": ([], C.c_char_p),
+    # internal test hook (csrc/test_hooks.cu), not part of include/coat.h
+    "coat_test_pack_prepare": ([_vp, _vp, _i64, C.c_double, _vp, _vp], _int),
     "coat_flags_to_status": ([C.c_uint32], _int),
     "coat_device_sm_count": ([], _int),
     "coat_encode_e4m3": ([_vp, _vp, _i64, _vp, _vp], _int),
@@ -102,6 +104,8 @@ def _load() -> C.CDLL:
             "There is no CPU fallback for the COAT hot path.")
     lib = C.CDLL(LIB_PATH)
     for name, (args, res) in _SIGS.items():
+        if name.startswith("coat_test_") and not hasattr(lib, name):
+            continue   # internal test hooks are optional (A/B builds of older sources)
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res

@@ -241,6 +241,163 @@ static __device__ __noinline__ PackParams pack_prepare_fast(uint32_t lo_bits, ui
     return p;
 }
 
+// ---------------------------------------------------------------------------
+// Low-latency pack_prepare: same results as pack_prepare_fast (and the
+// reference), bit for bit, as one straight-line FP64/FP32 block.
+//
+// pack_prepare_fast is ~320 dependent instructions (libdevice sqrt / div / log
+// with their special-case branches, and the k == 1 and k != 1 scale paths
+// serialised by divergence): ~2800 cycles per round on the pack warp, which the
+// element warps wait for.  Here every quantity is computed by an approximation
+// whose error is bounded well inside what decides the rounded result, and the
+// rounding is certified; lanes whose certification fails, or whose inputs are
+// special (0, Inf/NaN, extreme ranges that select mode 2), recompute with
+// pack_prepare_fast behind a warp vote.
+//   c  = (float)sqrt(lo*hi): lo*hi is exact in double; Goldschmidt sqrt from
+//        rsqrt.approx (~2^-52); float rounding certified by the 29 dropped
+//        mantissa bits being >= 16 double-ulps from the float midpoint.
+//   k  = (float)clamp(log_target / log(hi/lo), 1, 20): log2(hi) - log2(lo) by
+//        the CTA table l2b[top 7 mantissa bits] + a degree-6 log2(1+u) series
+//        (|u| < 2^-7; ~2^-51 absolute), k = (log_target/ln2) / L2 (~2^-49
+//        relative, vs ~2^-50 between the reference's own double k and the exact
+//        value); the clamp decisions and the float rounding are certified with a
+//        2^-43 margin.
+//   1/c, hi/c: quotients of 24-bit significands are >= 2^-48 (relative) away
+//        from any float midpoint, so a double value within 2^-51 rounds to the
+//        correctly rounded float: RN(1/c) and expand(hi) = RN(hi/c) are exact.
+//   group_scale: am/448 = am/(7*2^6) is >= 2^-27.8 (relative) from any float
+//        midpoint for normal quotients (the bits past the 24th repeat with
+//        period 3), so (float)(am * RN64(1/448)) == RN32(am/448); tiny am
+//        (< 2^-90, which lead to mode 2 anyway) fall back.
+//   1/s: s has an 8-bit significand, 1/s is >= 2^-33 from a float midpoint; one
+//        float Newton step from rcp.approx is within 2^-46, hence RN(1/s).
+//   k != 1: the SFU evaluation of expand(hi) certified exactly as in
+//        pack_prepare_fast (both ends of a 2^-15 interval give the same scale).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double rsqrt_seed_f64(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ double rcp_seed_f64(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx_f32(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// |low 29 mantissa bits - half| of a double: distance (in double ulps) of its
+// value from the nearest float rounding midpoint (normal float range).
+__device__ __forceinline__ uint32_t f32_mid_dist(double v) {
+    const int32_t low = int32_t(uint32_t(__double2loint(v)) & 0x1FFFFFFFu) - 0x10000000;
+    return uint32_t(low < 0 ? -low : low);
+}
+// 1/x to ~2^-52 relative (x normal, not huge): seed + 2 Newton steps.
+__device__ __forceinline__ double rcp_f64_fast(double x) {
+    double r = rcp_seed_f64(x);
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+// log2 pieces of a positive normal double v: returns E and the fractional part
+// log2(mantissa) = l2b[i] + P(u) to ~2^-52 absolute.
+__device__ __forceinline__ double log2_frac(double v, int& E, const CtaTables& T) {
+    const int hw = __double2hiint(v);
+    E = ((hw >> 20) & 0x7FF) - 1023;
+    const int i = (hw >> 13) & 0x7F;
+    const double m = __hiloint2double((hw & 0x000FFFFF) | 0x3FF00000, __double2loint(v));
+    const double ci = 1.0 + (double)i * 0.0078125;          // exact
+    const double d = m - ci;                                 // exact, [0, 2^-7)
+    // u = d / ci: float seed of 1/ci (2^-23) + one FP64 Newton step (2^-46); |u| < 2^-7
+    double r = (double)rcp_approx_f32(__double2float_rn(ci));
+    r = fma(r, fma(-ci, r, 1.0), r);
+    const double u = d * r;
+    // log2(1+u) = sum_k (-1)^(k+1) u^k / (k ln2), k <= 6 (truncation < 2^-52)
+    constexpr double c1 = 1.4426950408889634, c2 = -0.72134752044448170, c3 = 0.48089834696298783,
+                     c4 = -0.36067376022224085, c5 = 0.28853900817779268, c6 = -0.24044917348149390;
+    double q = fma(c6, u, c5);
+    q = fma(q, u, c4);
+    q = fma(q, u, c3);
+    q = fma(q, u, c2);
+    q = fma(q, u, c1);
+    return fma(q, u, T.l2b[i]);
+}
+
+static __device__ __noinline__ PackParams pack_prepare_slow(uint32_t lo_bits, uint32_t hi_bits, double log_target) {
+    return pack_prepare_fast(lo_bits, hi_bits, log_target);
+}
+
+// log2_target = log_target / ln2 (double).  Must be called by all 32 lanes
+// (warp vote); give idle lanes any finite positive extrema.
+__device__ __forceinline__ PackParams pack_prepare_lowlat(uint32_t lo_bits, uint32_t hi_bits, double log_target,
+                                                          double log2_target, const CtaTables& T) {
+    const float lo = u2f(lo_bits), hi = u2f(hi_bits);
+    const double lod = (double)lo, hid = (double)hi;
+    bool ok = hi_bits - 1u < 0x7F7FFFFFu && lo_bits - 1u < 0x7F7FFFFFu;   // both finite and > 0
+    // ---- c = (float)sqrt(lo * hi)
+    const double x = lod * hid;                              // exact
+    const double y0 = rsqrt_seed_f64(x);
+    double sq = x * y0, h = 0.5 * y0;
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+        const double rr = fma(-sq, h, 0.5);
+        sq = fma(sq, rr, sq);
+        h = fma(h, rr, h);
+    }
+    sq = fma(fma(-sq, sq, x), h, sq);
+    ok &= sq >= 0x1p-100 && sq <= 0x1p100 && f32_mid_dist(sq) > 16u;
+    const float c = __double2float_rn(sq);
+    const double cd = (double)c;
+    // ---- k
+    int eh, el;
+    const double fh = log2_frac(hid, eh, T), fl = log2_frac(lod, el, T);
+    const double L2 = (double)(eh - el) + (fh - fl);
+    ok &= L2 < 199.0;                                        // range > 2^200 selects mode 2
+    double ka = hi_bits == lo_bits ? 0.0 : log2_target * rcp_f64_fast(fmax(L2, 0x1p-60));
+    constexpr double kM = 0x1p-40;
+    const bool k_lo = ka <= 1.0 - kM, k_hi = ka >= kKMax * (1.0 + kM);
+    const bool k_mid = ka >= 1.0 + kM && ka <= kKMax * (1.0 - kM);
+    ok &= k_lo || k_hi || (k_mid && f32_mid_dist(ka) > 512u);
+    const float k = k_lo ? 1.0f : k_hi ? (float)kKMax : __double2float_rn(ka);
+    // ---- 1/c and expand(hi) for k == 1
+    const double rcd = rcp_f64_fast(cd);
+    const float inv_c = __double2float_rn(rcd);
+    const double am1d = hid * rcd;
+    // ---- k != 1: SFU evaluation of expand(hi), certified through the BF16 scale
+    const float rq = __fmul_rn(hi, inv_c);
+    const float e = ex2_approx(__fmul_rn(k, lg2_approx(rq)));
+    const float e_lo = __fmul_rn(e, 1.0f - kRelMufu), e_hi = __fmul_rn(e, 1.0f + kRelMufu);
+    const bool lin = k == 1.0f;
+    ok &= am1d < 0x1p127 || !lin;
+    const double am1 = (double)__double2float_rn(am1d);   // expand(hi) = RN32(hi / c), exact
+    const double aml = lin ? am1 : (double)e_lo, amh = lin ? am1 : (double)e_hi;
+    ok &= aml >= 0x1p-90 && amh < 0x1p127;
+    constexpr double kInv448 = 1.0 / 448.0;
+    const float s = round_bf16(__double2float_rn(aml * kInv448));
+    ok &= s == round_bf16(__double2float_rn(amh * kInv448)) && s >= 0x1p-100f;
+    // ---- 1/s (s: 8-bit significand)
+    const float r0 = rcp_approx_f32(s);
+    const float inv_s = __fmaf_rn(r0, __fmaf_rn(-s, r0, 1.0f), r0);
+    PackParams p;
+    p.k = k;
+    p.c = c;
+    p.s = s;
+    p.inv_c = inv_c;
+    p.inv_s = inv_s;
+    p.mode = lin ? 0 : 1;
+    p.bad = false;
+    if (__any_sync(0xFFFFFFFFu, !ok)) {
+        if (!ok) p = pack_prepare_slow(lo_bits, hi_bits, log_target);
+    }
+    return p;
+}
+
 // Codes of 4 values of one group; bit i of `unsure` marks an element that
 // needs the literal formula.  x must not be -0 (callers canonicalize).  The
 // lg2/ex2 inputs are never subnormal here (r in [2^-9, 2^9] for k > 1), so

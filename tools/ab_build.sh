@@ -8,10 +8,12 @@ OUT=$ROOT/build_ab/$NAME
 mkdir -p $OUT/obj
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="-O3 -std=c++17 $ARCH -lineinfo --fmad=false -prec-div=true -prec-sqrt=true -ftz=false -Xcompiler -fPIC -Xcompiler -ffp-contract=off -I$ROOT/include $*"
+pids=()
 for f in $ROOT/paper_2410_19313_b200/csrc/*.cu; do
   nvcc $FLAGS -c -o $OUT/obj/$(basename $f .cu).o $f &
+  pids+=($!)
 done
-wait
+for p in "${pids[@]}"; do wait $p || { echo "compile failed"; exit 1; }; done
 nvcc $ARCH -shared -o $OUT/libcoat.so $OUT/obj/*.o -lcudart
 rm -rf $OUT/obj
 echo built $OUT/libcoat.so
