@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--mgaq-branches", type=int, default=3,
+                    help="graph impl: records spread over this many parallel graph branches")
     ap.add_argument("--mgaq-impl", default="graph", choices=["batch", "graph"],
                     help="batch: coat_quantize_batch (one cooperative launch per layer); graph: the 9 "
                          "per-tensor entry points replayed as a CUDA graph")
@@ -430,14 +432,17 @@ def run_mgaq(args):
             scales = torch.empty(1, dtype=torch.int16, device=dev)
             alg_bytes += r * c * (2 + 1)
         bufs.append((name, r, c, G, x, codes, scales))
-    amax = torch.zeros(1, dtype=torch.int32, device=dev)
+    amax = torch.zeros(len(bufs), dtype=torch.int32, device=dev)   # one Group Scaling word per record
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     nel = sum(r * c for _, r, c, *_ in bufs)
 
-    def step(record=None):
+    def step(record=None, streams=None):
+        """The nine records; with `streams`, record i goes to streams[i % K]
+        (independent records overlap one kernel's tail with the next's ramp)."""
         launches = 0
-        s = torch.cuda.current_stream()
-        for name, r, c, G, x, codes, scales in bufs:
+        for i, (name, r, c, G, x, codes, scales) in enumerate(bufs):
+            s = streams[i % len(streams)] if streams else torch.cuda.current_stream()
+            am = amax.data_ptr() + 4 * i
             if record is not None:
                 record[name][0].record(s)
             if G:
@@ -445,8 +450,8 @@ def run_mgaq(args):
                                                flags.data_ptr(), s.cuda_stream)
                 launches += 1
             else:
-                st = L.coat_group_scale_max(x.data_ptr(), 1, r, c, 128, None, amax.data_ptr(), s.cuda_stream)
-                st = st or L.coat_quantize_per_tensor(x.data_ptr(), 1, r * c, amax.data_ptr(), codes.data_ptr(),
+                st = L.coat_group_scale_max(x.data_ptr(), 1, r, c, 128, None, am, s.cuda_stream)
+                st = st or L.coat_quantize_per_tensor(x.data_ptr(), 1, r * c, am, codes.data_ptr(),
                                                       scales.data_ptr(), flags.data_ptr(), s.cuda_stream)
                 launches += 3   # memset + amax + quant
             if record is not None:
@@ -472,13 +477,37 @@ def run_mgaq(args):
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         graph = torch.cuda.CUDAGraph()
+        nb = max(1, args.mgaq_branches)
+        branches = [torch.cuda.Stream() for _ in range(nb - 1)]
         with torch.cuda.stream(side):
             step()   # warm the capture stream
             torch.cuda.synchronize()
             with torch.cuda.graph(graph, stream=side):
-                launches_per_step = step()
+                if nb == 1:
+                    launches_per_step = step()
+                else:   # fork the records over nb branches of the graph, join at the end
+                    fork = torch.cuda.Event()
+                    fork.record(side)
+                    for b in branches:
+                        b.wait_event(fork)
+                    launches_per_step = step(streams=[side] + branches)
+                    for b in branches:
+                        j = torch.cuda.Event()
+                        j.record(b)
+                        side.wait_event(j)
         torch.cuda.synchronize()
         run_once = graph.replay
+        # the branched graph must reproduce the single-stream records bit for bit
+        step()
+        torch.cuda.synchronize()
+        ref = [(codes.clone(), scales.clone()) for *_, codes, scales in bufs]
+        for *_, codes, scales in bufs:
+            codes.zero_()
+            scales.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        for (name, *_, codes, scales), (rc, rs) in zip(bufs, ref):
+            assert torch.equal(codes, rc) and torch.equal(scales, rs), f"graph record {name} differs"
     else:
         launches_per_step = 2
         run_once = batch_step
@@ -509,7 +538,7 @@ def run_mgaq(args):
         "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
         "config": {"workload": "cfg2: MGAQ of one Llama-2-7B decoder layer, B4 x S2048 x H4096, I=11008",
                    "impl": "coat_quantize_batch (1 cooperative launch)" if args.mgaq_impl == "batch"
-                           else "9 entry points as one CUDA graph",
+                           else f"9 entry points as one CUDA graph, {args.mgaq_branches} parallel branch(es)",
                    "tensors": [t[:4] for t in MGAQ_TENSORS], "elements": nel,
                    "l2": "per-tensor inputs of 64-180 MB: stage-2 re-read partly L2-resident"},
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
