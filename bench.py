@@ -205,9 +205,15 @@ def main():
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
+    local = local % torch.cuda.device_count()   # (functional runs of N ranks on fewer GPUs)
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink; COAT_BENCH_BACKEND=gloo only for functional runs on one GPU
+        backend = os.environ.get("COAT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2410_19313_b200 import _lib
     L = _lib.lib
 
@@ -269,13 +275,26 @@ def main():
             raise RuntimeError(L.coat_last_error())
         cur[0] = 1 - i
 
+    flag_bits = torch.zeros(5, dtype=torch.int32, device=dev)
+
     def step(record=None):
-        if ws > 1:
-            dist.reduce_scatter_tensor(g, g_full)
+        """The sharded optimizer step: K1 on this rank's shard of
+        the state, plus (N > 1) the all-reduce of the 5-bit error word every
+        rank needs for the reference's commit semantics (zero.py).  The shards
+        are independent units: no data-path collective."""
         k1(record)
         if ws > 1:
-            dist.all_gather_into_tensor(w_full, w[cur[0]])
+            dist.all_reduce(flag_bits, op=dist.ReduceOp.MAX)
 
+    def zero_step():
+        """The full ZeRO step around it: gradient reduce-scatter (fp32, sum) ->
+        K1 on the shard -> parameter all-gather (zero.py ZeroAdamW)."""
+        dist.reduce_scatter_tensor(g, g_full)
+        step()
+        dist.all_gather_into_tensor(w_full, w[cur[0]])
+
+    if ws > 1:
+        dist.reduce_scatter_tensor(g, g_full)   # this rank's gradient shard (sum over ranks)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -304,6 +323,28 @@ def main():
     fl = int(flags.item())
     assert fl == 0, f"device flags 0x{fl:x}"
 
+    # ---- N > 1: the same steps with the ZeRO collectives around them, reported beside
+    zero = None
+    if ws > 1:
+        for _ in range(2):
+            zero_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        z0.record(stream)
+        for _ in range(args.steps):
+            zero_step()
+        z1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        zt = torch.tensor([z0.elapsed_time(z1) / args.steps], device=dev)
+        dist.all_reduce(zt, op=dist.ReduceOp.MAX)
+        zms = float(zt[0])
+        zero = {"ms_per_step": zms, "value": P / (zms * 1e-3), "unit": "params/s",
+                "collectives": f"{dist.get_backend()} reduce_scatter(g fp32, sum) + all_gather(w fp32) "
+                               "around each step",
+                "bytes_per_rank_per_step": int(2 * 4 * P * (ws - 1) / ws)}
+
     # ---- end to end through the C-ABI with HOST buffers (pinned), state in HBM
     e2e = None
     if not args.no_e2e:
@@ -331,12 +372,14 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "params_total": P, "params_per_rank": n,
-                       "group": GROUP, "parallelism": f"zero-dp{ws}",
+                       "group": GROUP, "parallelism": f"zero-dp{ws}" + ("" if ws == 1 else
+                                                                         " (state shards, no data-path collective)"),
                        "state": "E4M3 codes + BF16 scale + fp32 (k, c) per 1x128 group, m and v",
                        "l2": f"inputs {BYTES_PER_PARAM * n / 1e9:.1f} GB per rank >> 126 MB L2 "
                              "(no flush needed)",
                        "collectives": "none (N=1)" if ws == 1 else
-                                      "NCCL reduce_scatter(g fp32) + all_gather(w fp32)"},
+                                      "all_reduce of the 5-bit error word per step; the ZeRO "
+                                      "reduce-scatter/all-gather are timed separately (zero_with_collectives)"},
             "kernel_ms": k_ms,
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -345,6 +388,7 @@ def main():
                          "algorithmic_bytes_per_param": BYTES_PER_PARAM},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "zero_with_collectives": zero,
             "clocks": sampler.summary(),
             # K1 on the whole rounds + the generic kernel on the n % round tail (if any);
             # round = 14 groups (COAT_K1_EW=8: 16, =6: 12) of 128 params (k1_ws.cu)
