@@ -63,7 +63,7 @@ def main():
             "warps_active_pct": val("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "pipe_alu_pct": val("TPC.TriageCompute.sm__inst_executed_pipe_alu_realtime.avg.pct_of_peak_sustained_elapsed"),
             "pipe_fp64_pct": val("TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
-            "pipe_tensor_pct": val("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+            "pipe_tensor_pct": val("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
             "lsu_wavefronts_pct": val("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
             "grid": val("launch__grid_size"),
             "block": val("launch__block_size"),
