@@ -510,7 +510,9 @@ def run_mgaq(args):
     def batch_step():
         st = L.coat_quantize_batch(items, len(bufs), flags.data_ptr(), torch.cuda.current_stream().cuda_stream)
         assert st == 0, L.coat_last_error()
-        return 2   # memset of the grid-barrier word + the cooperative kernel
+        if os.environ.get("COAT_MGAQ_BATCH", "").startswith("c"):
+            return 2   # memset of the grid-barrier word + the cooperative kernel
+        return sum(1 if G else 3 for _, _, _, G in MGAQ_TENSORS)   # per record: kernel(s) (+ memset)
 
     for _ in range(args.warmup):
         step()
@@ -553,7 +555,8 @@ def run_mgaq(args):
         for (name, *_, codes, scales), (rc, rs) in zip(bufs, ref):
             assert torch.equal(codes, rc) and torch.equal(scales, rs), f"graph record {name} differs"
     else:
-        launches_per_step = 2
+        launches_per_step = batch_step()
+        torch.cuda.synchronize()
         run_once = batch_step
     evs = {name: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for name, *_ in MGAQ_TENSORS}
@@ -581,7 +584,9 @@ def run_mgaq(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
         "config": {"workload": "cfg2: MGAQ of one Llama-2-7B decoder layer, B4 x S2048 x H4096, I=11008",
-                   "impl": "coat_quantize_batch (1 cooperative launch)" if args.mgaq_impl == "batch"
+                   "impl": ("coat_quantize_batch (" + ("1 cooperative launch" if os.environ.get(
+                       "COAT_MGAQ_BATCH", "").startswith("c") else "3 internal streams") + ")")
+                           if args.mgaq_impl == "batch"
                            else f"9 entry points as one CUDA graph, {args.mgaq_branches} parallel branch(es)",
                    "tensors": [t[:4] for t in MGAQ_TENSORS], "elements": nel,
                    "l2": "per-tensor inputs of 64-180 MB: stage-2 re-read partly L2-resident"},

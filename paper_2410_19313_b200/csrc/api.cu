@@ -167,7 +167,8 @@ coat_status coat_quantize_batch(const coat_mgaq_item* items, int32_t n_items, ui
             return fail(COAT_ERR_INVALID, "quantize_batch: needs numel % 16 == 0, 32-byte aligned x, 16-byte aligned codes");
         it[i] = MgaqItem{m.x, (int)m.dtype, n, G, m.codes, m.scales, m.d_amax_bits};
     }
-    return cuda_status(launch_mgaq_batch(it, n_items, d_flags, S(stream)));
+    return cuda_status(mgaq_batch_cooperative() ? launch_mgaq_batch(it, n_items, d_flags, S(stream))
+                                                : launch_mgaq_streams(it, n_items, d_flags, S(stream)));
 }
 
 // ------------------------------------------------------- fused producers -----

@@ -94,6 +94,8 @@ struct MgaqItem {
     uint32_t* amax_out;     // per-tensor: fp32 absmax bits (may be NULL)
 };
 cudaError_t launch_mgaq_batch(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t stream);
+cudaError_t launch_mgaq_streams(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t stream);
+bool mgaq_batch_cooperative();
 
 // fused producers (producers.cu)
 struct RmsBlockArgs {
