@@ -218,6 +218,32 @@ coat_status coat_adamw_dre_step_host(const float* w_host_in, float* w_host_out, 
                                      coat_moment_state v_out, const coat_adamw_config* cfg,
                                      int64_t t, uint32_t* d_flags, int64_t chunk, void* stream);
 
+/* ------------------------------------------------------ ZeRO step (NCCL) -- */
+/* The ZeRO-sharded step (paper_2410_19313_b200/zero.py is the
+ * torch.distributed form).  One process per GPU, comm = this rank's
+ * ncclComm_t (as void*) of nranks ranks.  w_full, g_full: the flat [n_total]
+ * fp32 buffers (FlatLayout: every tensor 128-aligned, n_total % (128*nranks) ==
+ * 0); this rank owns [rank*n, (rank+1)*n), n = n_total / nranks, and only that
+ * shard's state (m_in, v_in -> m_out, v_out as in coat_adamw_dre_step).
+ * g_shard, w_scratch: n-float device scratch.  Stream-ordered, no host sync:
+ * reduce-scatter (sum) g_full -> g_shard; the fused step on the shard into
+ * w_scratch; all-reduce of the error word so *d_flags (zeroed by the caller)
+ * is the OR over all ranks; when the step must change nothing
+ * (NonFiniteGradient, contract NonFiniteInput) the old shard is republished;
+ * all-gather w_scratch -> w_full.  After a sync the caller commits m_out,
+ * v_out by coat_flags_to_status exactly as for the single-GPU step.  NCCL is
+ * loaded at run time (libnccl.so.2); COAT_ERR_NCCL if absent or failing. */
+coat_status coat_zero_step(float* w_full, const float* g_full, int64_t n_total, int64_t group_size,
+                           coat_moment_state m_in, coat_moment_state v_in, coat_moment_state m_out,
+                           coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t, float* g_shard,
+                           float* w_scratch, uint32_t* d_flags, void* nccl_comm, int32_t rank, int32_t nranks,
+                           void* stream);
+/* Communicator helpers for callers without their own NCCL binding: rank 0
+ * creates the 128-byte id, every rank passes it to coat_nccl_comm_init. */
+coat_status coat_nccl_unique_id(uint8_t* out_id /* 128 bytes */);
+coat_status coat_nccl_comm_init(void** nccl_comm, int32_t nranks, const uint8_t* id, int32_t rank);
+coat_status coat_nccl_comm_destroy(void* nccl_comm);
+
 /* ----------------------------------------------------------- FP8 linear -- */
 /* The reference's linear (flow.cpp:21-46, no public entry point; SURVEY.md 8(a)
  * a18) on tcgen05/TMEM/TMA.  W is (K, N) row-major as in flow.hpp:44-47.

@@ -60,6 +60,11 @@ _SIGS = {
     "coat_version": ([], C.c_char_p),
     "coat_status_string": ([_int], C.c_char_p),
     "coat_last_error": ([], C.c_char_p),
+    "coat_zero_step": ([_vp, _vp, _i64, _i64, MomentState, MomentState, MomentState, MomentState, _vp, _i64,
+                        _vp, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp], _int),
+    "coat_nccl_unique_id": ([_vp], _int),
+    "coat_nccl_comm_init": ([_vp, C.c_int32, _vp, C.c_int32], _int),
+    "coat_nccl_comm_destroy": ([_vp], _int),
     # internal test hook (csrc/test_hooks.cu), not part of include/coat.h
     "coat_test_pack_prepare": ([_vp, _vp, _i64, C.c_double, _vp, _vp], _int),
     "coat_flags_to_status": ([C.c_uint32], _int),

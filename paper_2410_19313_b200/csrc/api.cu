@@ -327,6 +327,59 @@ coat_status coat_adamw_dre_step_host(const float* w_host_in, float* w_host_out, 
                                            d_flags, g_fallback_counter, chunk, S(stream)));
 }
 
+// ------------------------------------------------------------- ZeRO (NCCL) --
+static coat_status nccl_status(int r, const char* what) {
+    if (r == 0) return COAT_OK;
+    std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, nccl_error_string(r));
+    return COAT_ERR_NCCL;
+}
+
+coat_status coat_nccl_unique_id(uint8_t* out_id) {
+    if (!out_id) return fail(COAT_ERR_INVALID, "nccl_unique_id: NULL");
+    if (!nccl_available()) return fail(COAT_ERR_NCCL, "NCCL library (libnccl.so.2) not found");
+    return nccl_status(nccl_unique_id(out_id), "ncclGetUniqueId");
+}
+
+coat_status coat_nccl_comm_init(void** comm, int32_t nranks, const uint8_t* id, int32_t rank) {
+    if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(COAT_ERR_INVALID, "nccl_comm_init: bad arguments");
+    if (!nccl_available()) return fail(COAT_ERR_NCCL, "NCCL library (libnccl.so.2) not found");
+    return nccl_status(nccl_comm_init(comm, nranks, id, rank), "ncclCommInitRank");
+}
+
+coat_status coat_nccl_comm_destroy(void* comm) {
+    if (!comm) return COAT_OK;
+    if (!nccl_available()) return fail(COAT_ERR_NCCL, "NCCL library (libnccl.so.2) not found");
+    return nccl_status(nccl_comm_destroy(comm), "ncclCommDestroy");
+}
+
+coat_status coat_zero_step(float* w_full, const float* g_full, int64_t n_total, int64_t G, coat_moment_state m_in,
+                           coat_moment_state v_in, coat_moment_state m_out, coat_moment_state v_out,
+                           const coat_adamw_config* cfg, int64_t t, float* g_shard, float* w_scratch,
+                           uint32_t* d_flags, void* comm, int32_t rank, int32_t nranks, void* stream) {
+    if (!w_full || !g_full || !g_shard || !w_scratch || !d_flags || !comm)
+        return fail(COAT_ERR_INVALID, "zero_step: NULL buffer or communicator");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COAT_ERR_INVALID, "zero_step: bad rank / nranks");
+    if (n_total <= 0 || n_total % (128 * int64_t(nranks)) != 0)
+        return fail(COAT_ERR_GEOMETRY, "zero_step: n_total must be a positive multiple of 128 * nranks (FlatLayout)");
+    if (!nccl_available()) return fail(COAT_ERR_NCCL, "NCCL library (libnccl.so.2) not found");
+    const int64_t n = n_total / nranks;
+    AdamWScalars a;
+    coat_status st = step_args(cfg, n, G, t, m_in, v_in, m_out, v_out, a);
+    if (st != COAT_OK) return st;
+    const cudaStream_t s = S(stream);
+    st = nccl_status(zero_reduce_scatter(g_full, g_shard, n, comm, s), "ncclReduceScatter");
+    if (st != COAT_OK) return st;
+    const float* w_own = w_full + int64_t(rank) * n;
+    st = cuda_status(launch_adamw_dre_step(w_own, w_scratch, g_shard, n, in_of(m_in), in_of(v_in), out_of(m_out),
+                                           out_of(v_out), a, d_flags, g_fallback_counter, s));
+    if (st != COAT_OK) return st;
+    cudaError_t ce = cudaSuccess;
+    st = nccl_status(zero_agree_and_select(d_flags, w_own, w_scratch, n, comm, s, &ce), "ncclAllReduce");
+    if (st != COAT_OK) return st;
+    if ((st = cuda_status(ce)) != COAT_OK) return st;
+    return nccl_status(zero_all_gather(w_scratch, w_full, n, comm, s), "ncclAllGather");
+}
+
 coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n, int64_t G,
                                 coat_moment_state m_in, coat_moment_state v_in, coat_moment_state m_out,
                                 coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t,

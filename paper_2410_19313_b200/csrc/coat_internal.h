@@ -154,4 +154,15 @@ cudaError_t launch_quantize_per_tensor(const void* x, int dtype, int64_t n,
                                        const uint32_t* amax_bits, uint8_t* codes,
                                        uint16_t* scale_out, uint32_t* flags, cudaStream_t stream);
 
+// ZeRO collectives (zero_nccl.cu); NCCL results as int (0 = ncclSuccess, -1 = no NCCL library)
+bool nccl_available();
+const char* nccl_error_string(int r);
+int nccl_unique_id(uint8_t* out128);
+int nccl_comm_init(void** comm, int nranks, const uint8_t* id128, int rank);
+int nccl_comm_destroy(void* comm);
+int zero_reduce_scatter(const float* g_full, float* g_shard, int64_t n_shard, void* comm, cudaStream_t st);
+int zero_all_gather(const float* w_shard, float* w_full, int64_t n_shard, void* comm, cudaStream_t st);
+int zero_agree_and_select(uint32_t* d_flags, const float* w_old, float* w_scratch, int64_t n_shard, void* comm,
+                          cudaStream_t st, cudaError_t* cuda_err);
+
 }  // namespace coat
