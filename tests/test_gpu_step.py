@@ -249,3 +249,37 @@ def test_step_in_place_state_matches_ping_pong(coat, port):
         for x, y in ((mi, mp[b]), (vi, vp[b])):
             for key in ("codes", "scales", "k", "c"):
                 assert torch.equal(x[key], y[key]), (t, key)
+
+
+@pytest.mark.parametrize("moment,group,k,code", [("m", 3, 1.0, 0x7F), ("m", 5, 2.5, 0xFF),
+                                                  ("v", 7, 3.0, 0x7F), ("v", 9, 1.0, 0xFF)])
+def test_nan_code_in_state_is_a_contract_error(coat, port, moment, group, k, code):
+    """A NaN E4M3 code in the stored state (0x7F / 0xFF) makes unpack (decode,
+    fp8.cpp:145-152) throw NonFiniteInput before anything is mutated -- for a
+    k == 1 group (exact contract) and a k != 1 group (table contract, where the
+    product itself would be finite), in m and in v; the reference agrees."""
+    import torch
+    n = 128 * 64
+    r = rng(51)
+    w0 = (r.standard_normal(n) * 0.02).astype(np.float32)
+    g0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
+    m, v = port.make_slot(n)
+    wr = w0.copy()
+    assert port.step(wr, g0, m, v, 0, CFG) == 0
+    st = {"m": m, "v": v}[moment]
+    st["codes"][group * 128 + 17] = code
+    st["k"][group] = np.float32(k)
+    slot = coat.make_slot([n])
+    slot.load_state(m, v, 1)
+    w = dev(wr)
+    g = dev((r.standard_normal(n) * 1e-3).astype(np.float32))
+    before = [t.clone() for t in (w, slot.m.quantized.codes, slot.v.quantized.codes, slot.m.k, slot.v.k)]
+    with pytest.raises(coat.NonFiniteInput):
+        coat.step(w, g, slot, coat.AdamWConfig(**CFG))
+    after = (w, slot.m.quantized.codes, slot.v.quantized.codes, slot.m.k, slot.v.k)
+    assert all(torch.equal(a, b) for a, b in zip(after, before))
+    assert slot.step == 1
+    # the reference throws NonFiniteInput as well and leaves w untouched
+    w_ref = wr.copy()
+    assert port.step(w_ref, host(g), m, v, 1, CFG) == 3
+    assert np.array_equal(w_ref, wr)
