@@ -141,16 +141,18 @@ def test_power_of_two_rescale_gpu(coat):
         assert np.array_equal(host(b.scales), np.ldexp(host(a.scales), sh))
 
 
-def test_llama_layer_sizes_bit_exact_sampled(coat, port):
-    """Config-2 shapes (8192 x 11008 bf16): GPU over the full tensor, oracle on
-    a row sample (groups are row-local, so rows are independent)."""
+def test_llama_layer_sizes_bit_exact_full(coat, port):
+    """Config-2 shapes at full size (8192 x 11008 bf16, 90M elements): every
+    code and scale of the per-group (1x16) quantization against the oracle, and
+    the per-tensor (Group Scaling) scale plus every code of it."""
     import torch
     rows, cols = 8192, 11008
     g = torch.Generator(device="cuda").manual_seed(3)
     xt = (torch.randn(rows, cols, device="cuda", generator=g) * 3).to(torch.bfloat16)
     xt[5] *= 50
+    xt[::97, ::13] = 0.0
     q = coat.quantize(xt, coat.QuantGeometry.per_group(16))
-    sample = [0, 5, 777, 4096, rows - 1]
+    sample = list(range(rows))
     xs = xt[sample].float().cpu().numpy()
     codes, scales = port.quantize(xs, 16)
     assert np.array_equal(host(q.codes[sample]), codes)
@@ -163,9 +165,25 @@ def test_llama_layer_sizes_bit_exact_sampled(coat, port):
     assert np.array_equal(host(qt.codes[sample]), exp)
 
 
+def test_quantize_batch_cooperative_kernel_matches_single_calls():
+    """The single cooperative launch behind COAT_MGAQ_BATCH=coop (chosen once
+    per process, hence a subprocess) gives the entry points' results too."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, COAT_MGAQ_BATCH="coop")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_quant.py"), "-k", "batch and not cooperative"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "passed" in r.stdout
+
+
 def test_quantize_batch_matches_single_calls(coat):
-    """coat_quantize_batch (one cooperative launch for a layer's MGAQ) is
-    bit-identical to the per-tensor entry points, mixed geometries and dtypes."""
+    """coat_quantize_batch (a layer's MGAQ records in one call: 3 internal
+    streams by default) is bit-identical to the per-tensor entry points, mixed
+    geometries and dtypes."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(3)
     specs = [((96, 256), torch.bfloat16, coat.QuantGeometry.per_group(16)),
