@@ -13,8 +13,9 @@
 // Three staging slots (w and g, `chunk` fp32 each) let chunk i+1 upload while
 // chunk i computes and chunk i-1 downloads.  Host buffers must be pinned
 // (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous.
-// Chunks are multiples of the 512-parameter warp tile, so every chunk starts
-// on a 1x128 group boundary and uses the state slice of its own groups.
+// Chunks are multiples of the fused kernel's round (k1_ws_round_params(): 14
+// groups of 128), so every chunk starts on a 1x128 group boundary, uses the
+// state slice of its own groups, and only the last one has a ragged tail.
 #include <cstdint>
 #include <mutex>
 
@@ -94,7 +95,8 @@ cudaError_t host_pipelined_step(const float* w_host_in, float* w_host_out, const
     if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
     std::lock_guard<std::mutex> lock(g_ws_mu);
     Workspace& ws = g_ws[dev];
-    chunk = (chunk + 511) / 512 * 512;
+    const int64_t unit = k1_ws_round_params();
+    chunk = (chunk + unit - 1) / unit * unit;
     e = ws.init(dev, chunk);
     if (e != cudaSuccess) return e;
 
