@@ -50,8 +50,8 @@ struct StepScalars {
 };
 
 struct WarpShared {
-    ContractParams cp[8];   // [moment*4 + group] of the incoming state
-    PackParams pp[8];       // [moment*4 + group] of the outgoing state
+    ContractParams cp[8];   // [moment*TG + group] of the incoming state
+    PackParams pp[8];       // [moment*TG + group] of the outgoing state
     uint32_t ext[16];       // lo/hi bit patterns per pair
 };
 
@@ -122,6 +122,7 @@ __device__ __forceinline__ void contract4(uint32_t codes, const ContractParams& 
 // ----------------------------------------------------------------------------
 // K1: fused step.
 // ----------------------------------------------------------------------------
+template <int TG>   // groups per warp tile (4; 1 for the short ragged tail after K1: 4x less serial work per lane)
 __global__ void __launch_bounds__(kThreads)
 adamw_dre_step_kernel(const float* w_in, float* w_out, const float* __restrict__ g, int64_t n,
                       MomentStateIn m_in, MomentStateIn v_in, MomentStateOut m_out,
@@ -132,7 +133,7 @@ adamw_dre_step_kernel(const float* w_in, float* w_out, const float* __restrict__
     const int wid = threadIdx.x >> 5;
     WarpShared& ws = shared[wid];
     const int64_t ng = (n + dre::kG - 1) / dre::kG;
-    const int64_t ntiles = (ng + kTileGroups - 1) / kTileGroups;
+    const int64_t ntiles = (ng + TG - 1) / TG;
     const int64_t warp_global = int64_t(blockIdx.x) * kWarps + wid;
     const int64_t warp_stride = int64_t(gridDim.x) * kWarps;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(w_in) | reinterpret_cast<uintptr_t>(w_out) |
@@ -141,21 +142,21 @@ adamw_dre_step_kernel(const float* w_in, float* w_out, const float* __restrict__
     uint32_t fallbacks = 0;
 
     for (int64_t tile = warp_global; tile < ntiles; tile += warp_stride) {
-        const int64_t g0 = tile * kTileGroups;
-        const int gvalid = (int)imin64(kTileGroups, ng - g0);
+        const int64_t g0 = tile * TG;
+        const int gvalid = (int)imin64(TG, ng - g0);
         const int64_t base = g0 * dre::kG;
-        const bool full = vec_ok && base + kTile <= n;
+        const bool full = vec_ok && base + TG * dre::kG <= n;
 
-        // ---- incoming per-group meta: lane p = mom*4 + grp
-        if (lane < 8) {
-            const int mom = lane >> 2, grp = lane & 3;
+        // ---- incoming per-group meta: lane p = mom*TG + grp
+        if (lane < 2 * TG) {
+            const int mom = lane / TG, grp = lane % TG;
             if (grp < gvalid) ws.cp[lane] = load_contract(mom ? v_in : m_in, g0 + grp);
         }
         // ---- streaming loads
-        float w[kTileGroups][4], gr[kTileGroups][4];
-        uint32_t cm[kTileGroups], cv[kTileGroups];
+        float w[TG][4], gr[TG][4];
+        uint32_t cm[TG], cv[TG];
 #pragma unroll
-        for (int j = 0; j < kTileGroups; ++j) {
+        for (int j = 0; j < TG; ++j) {
             const int64_t e0 = base + j * dre::kG + 4 * lane;
             if (j < gvalid) {
                 cm[j] = ldg_u32(m_in.codes + e0);
@@ -180,13 +181,13 @@ adamw_dre_step_kernel(const float* w_in, float* w_out, const float* __restrict__
         __syncwarp();
 
         // ---- unpack (dequantize + contract) and AdamW
-        float m[kTileGroups][4], v[kTileGroups][4];
+        float m[TG][4], v[TG][4];
         bool bad_state = false;
 #pragma unroll
-        for (int j = 0; j < kTileGroups; ++j) {
+        for (int j = 0; j < TG; ++j) {
             if (j < gvalid) {
                 contract4(cm[j], ws.cp[j], m[j], bad_state);
-                contract4(cv[j], ws.cp[4 + j], v[j], bad_state);
+                contract4(cv[j], ws.cp[TG + j], v[j], bad_state);
             } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) m[j][i] = v[j][i] = 0.0f;
@@ -201,30 +202,30 @@ adamw_dre_step_kernel(const float* w_in, float* w_out, const float* __restrict__
         if (bad_state) myflags |= kFlagContract;
 
         // ---- group extrema (exact) for both moments: 16 redux.sync
-        uint32_t lo[8], hi[8];
+        uint32_t lo[2 * TG], hi[2 * TG];
 #pragma unroll
-        for (int j = 0; j < kTileGroups; ++j) {
+        for (int j = 0; j < TG; ++j) {
             uint32_t l, h;
             extrema4(m[j], l, h);
             lo[j] = warp_min_u32(l);
             hi[j] = warp_max_u32(h);
             extrema4(v[j], l, h);
-            lo[4 + j] = warp_min_u32(l);
-            hi[4 + j] = warp_max_u32(h);
+            lo[TG + j] = warp_min_u32(l);
+            hi[TG + j] = warp_max_u32(h);
         }
         if (lane == 0) {
 #pragma unroll
-            for (int p = 0; p < 8; ++p) {
+            for (int p = 0; p < 2 * TG; ++p) {
                 ws.ext[2 * p] = lo[p];
                 ws.ext[2 * p + 1] = hi[p];
             }
         }
         __syncwarp();
-        pack_params_pass(ws, lane, 8, S.log_target);
+        pack_params_pass(ws, lane, 2 * TG, S.log_target);
 
         // ---- outgoing meta (lanes 0..7) + codes + weights
-        if (lane < 8) {
-            const int mom = lane >> 2, grp = lane & 3;
+        if (lane < 2 * TG) {
+            const int mom = lane / TG, grp = lane % TG;
             if (grp < gvalid) {
                 const PackParams& p = ws.pp[lane];
                 store_pack(mom ? v_out : m_out, g0 + grp, p);
@@ -232,11 +233,11 @@ adamw_dre_step_kernel(const float* w_in, float* w_out, const float* __restrict__
             }
         }
 #pragma unroll
-        for (int j = 0; j < kTileGroups; ++j) {
+        for (int j = 0; j < TG; ++j) {
             const int64_t e0 = base + j * dre::kG + 4 * lane;
             if (j < gvalid) {
                 stg_u32(m_out.codes + e0, pack4(m[j], ws.pp[j], fallbacks));
-                stg_u32(v_out.codes + e0, pack4(v[j], ws.pp[4 + j], fallbacks));
+                stg_u32(v_out.codes + e0, pack4(v[j], ws.pp[TG + j], fallbacks));
             }
             if (full) {
                 stg_stream_f4(w_out + e0, make_float4(w[j][0], w[j][1], w[j][2], w[j][3]));
@@ -419,8 +420,15 @@ cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* 
     const MomentStateOut vo{v_out.codes + done, v_out.scales + gdone, v_out.k + gdone, v_out.c + gdone};
     const int64_t rest = n - done;
     const int64_t ng = (rest + dre::kG - 1) / dre::kG;
+    if (done > 0 && ng <= 64) {
+        // the ragged tail after K1 (< one round): one group per warp, so the
+        // per-element literal paths run 4x shorter chains (~40 -> ~10 us)
+        adamw_dre_step_kernel<1><<<grid_for(ng, kWarps), kThreads, 0, stream>>>(
+            w_in + done, w_out + done, g + done, rest, mi, vi, mo, vo, S, flags, fallbacks);
+        return cudaGetLastError();
+    }
     const int64_t ntiles = (ng + kTileGroups - 1) / kTileGroups;
-    adamw_dre_step_kernel<<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(
+    adamw_dre_step_kernel<kTileGroups><<<grid_for(ntiles, kWarps), kThreads, 0, stream>>>(
         w_in + done, w_out + done, g + done, rest, mi, vi, mo, vo, S, flags, fallbacks);
     return cudaGetLastError();
 }
