@@ -22,7 +22,8 @@ def _bf16(a):
     return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("rows,h,dtype", [(96, 4096, "bf16"), (33, 512, "fp32"), (8, 11008, "bf16")])
+@pytest.mark.parametrize("rows,h,dtype", [(96, 4096, "bf16"), (33, 512, "fp32"), (8, 11008, "bf16"),
+                                          (8192, 4096, "bf16")])   # the last: cfg2's full rmsnorm input
 def test_rmsnorm_block_bit_exact_vs_oracle(coat, port, rows, h, dtype):
     import torch
     x = port.generate(1, (rows, h), 0.05, 30.0, 11)
@@ -52,7 +53,7 @@ def test_rmsnorm_block_matches_reference_layer_tape(coat, ref):
     assert np.array_equal(_np(qy.codes).reshape(-1), c_q) and np.array_equal(_np(qy.scales), s_q)
 
 
-@pytest.mark.parametrize("rows,cols", [(64, 11008), (40, 512)])
+@pytest.mark.parametrize("rows,cols", [(64, 11008), (40, 512), (8192, 11008)])   # the last: cfg2 full size
 def test_silu_mul_block(coat, port, rows, cols):
     import torch
     g = _bf16(port.generate(1, (rows, cols), 0.02, 8.0, 21) * np.float32(2.0))
@@ -73,3 +74,26 @@ def test_silu_mul_block(coat, port, rows, cols):
     sc, ss = port.quantize(port.silu(port.dequantize(gc, gs, 16)), 16)
     diff = np.count_nonzero(_np(qs.codes) != sc) / sc.size
     assert diff < 1e-3, diff
+
+
+def test_rmsnorm_block_signed_zeros(coat, port):
+    """x values that quantize to -0 (code 0x80: a tiny negative next to a large
+    group max) give x_used = -0 and rmsnorm -0 / rms * w = -0 (flow.cpp:56-71);
+    the division's fast path must keep the sign (found at cfg2's full size)."""
+    import torch
+    rows, h = 16, 256
+    x = port.generate(1, (rows, h), 0.0, 1.0, 31)
+    x[:, ::16] = 300.0                       # each 1x16 group's max
+    x[:, 1::16] = -1e-6                      # -> code 0x80 after quantization
+    x[:, 2::16] = 1e-6                       # -> code 0x00
+    xt = _bf16(x).cuda()
+    x = xt.float().cpu().numpy()
+    w = np.linspace(0.5, 1.5, h).astype(np.float32)
+    w[5::7] *= -1.0                          # negative weights flip the zero's sign
+    qx, qy, rms, y = coat.rmsnorm_quantize(xt, torch.from_numpy(w), eps=1e-6, return_y=True)
+    xc, xs = port.quantize(x, 16)
+    assert (xc == 0x80).any()
+    y_ref = port.rmsnorm(port.dequantize(xc, xs, 16), w, 1e-6)
+    assert np.array_equal(_np(y).view(np.uint32), y_ref.view(np.uint32))
+    yc, ys = port.quantize(y_ref, 0)
+    assert np.array_equal(_np(qy.codes), yc) and np.array_equal(_np(qy.scales), ys)
