@@ -7,7 +7,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("rows,cols,G", [(100, 256, 16), (64, 4096, 0), (333, 128, 128), (7, 48, 16)])
+@pytest.mark.parametrize("rows,cols,G", [(100, 256, 16), (64, 4096, 0), (333, 128, 128), (7, 48, 16),
+                                         (8192, 4096, 0), (8192, 5120, 0), (8192, 11008, 16)])   # full sizes
 @pytest.mark.parametrize("odt", ["fp32", "bf16"])
 def test_used_values_transposed(coat, port, rows, cols, G, odt):
     import torch
@@ -25,7 +26,7 @@ def test_used_values_transposed(coat, port, rows, cols, G, odt):
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
 
 
-@pytest.mark.parametrize("n", [8192 * 64, 1000 * 16 + 7])
+@pytest.mark.parametrize("n", [8192 * 64, 1000 * 16 + 7, 8192 * 4096])   # the last: attn.out at full size
 def test_requantize_cached(coat, port, n):
     import torch
     x = port.generate(1, (n,), 0.05, 30.0, 6)
