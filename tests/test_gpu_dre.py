@@ -46,6 +46,8 @@ def special_groups():
     x = rng(5).standard_normal(128).astype(np.float32); x[::3] = 0; g.append(x)
     tiny = np.geomspace(1e-38, 1e-36, 128).astype(np.float32); g.append(tiny)   # tiny scales
     big = np.geomspace(1e30, 3e38, 128).astype(np.float32); g.append(big)
+    g.append(np.full(128, -0.0, np.float32))                   # all -0 (expand_one(-0) = +0)
+    x = rng(6).standard_normal(128).astype(np.float32); x[1::4] = -0.0; g.append(x)   # -0 among values
     return np.concatenate(g)
 
 
@@ -89,6 +91,13 @@ def test_expand_quantize_large_random(coat, port):
     x = np.concatenate([np.exp(r.uniform(-0.5 * np.log(q), 0.5 * np.log(q), 128))
                         * r.choice([-1, 1], 128) * 10 ** r.uniform(-9, 2) for q in ranges])
     _check_state(coat, port, x.astype(np.float32))
+
+
+def test_expand_quantize_cfg1_size(coat, port):
+    """cfg1's 16 Mi-element moment tensors (131,072 groups), m-like and v-like."""
+    groups = 1 << 17
+    _check_state(coat, port, m_like(port, groups, seed=41))
+    _check_state(coat, port, v_like(groups, seed=42))
 
 
 def test_fallback_rate_is_small(coat, port):

@@ -283,3 +283,33 @@ def test_nan_code_in_state_is_a_contract_error(coat, port, moment, group, k, cod
     w_ref = wr.copy()
     assert port.step(w_ref, host(g), m, v, 1, CFG) == 3
     assert np.array_equal(w_ref, wr)
+
+
+def test_step_signed_zero_weights_and_grads(coat, port):
+    """w and g containing +0 and -0 (and groups of them) step exactly like
+    the reference: the signs of zero updates follow IEEE as in adamw_update
+    (optimizer.cpp:57-68), zero moments pack to +0 (expand.cpp:18-22)."""
+    import torch
+    n = 128 * 96
+    r = rng(71)
+    w0 = (r.standard_normal(n) * 0.02).astype(np.float32)
+    w0[::7] = 0.0
+    w0[3::7] = -0.0
+    w0[128 * 5:128 * 6] = -0.0
+    m, v = port.make_slot(n)
+    slot = coat.make_slot([n])
+    w_ref, w = w0.copy(), dev(w0)
+    c = coat.AdamWConfig(**CFG)
+    for t in range(3):
+        g = (r.standard_normal(n) * 1e-3).astype(np.float32)
+        g[::5] = -0.0
+        g[2::5] = 0.0
+        g[128 * 7:128 * 9] = -0.0
+        assert port.step(w_ref, g, m, v, t, CFG) == 0
+        coat.step(w, dev(g), slot, c)
+        wd = host(w)
+        bad = np.nonzero(wd.view(np.uint32) != w_ref.view(np.uint32))[0]
+        assert bad.size == 0, (t, bad[:8], wd[bad[:8]], w_ref[bad[:8]])
+        gm, gv = gpu_state(slot)
+        assert_state_equal(gm, m, f"m step {t}")
+        assert_state_equal(gv, v, f"v step {t}")
