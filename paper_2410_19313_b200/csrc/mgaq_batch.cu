@@ -268,12 +268,14 @@ bool mgaq_batch_cooperative() {
 cudaError_t launch_mgaq_streams(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     if (n > kMgaqMaxItems) return cudaErrorInvalidValue;
-    static StreamSet ss;
+    static StreamSet sets[16];              // per device, created on first use
     static std::mutex mu;
-    std::lock_guard<std::mutex> lock(mu);   // the stream set is shared by all callers
+    std::lock_guard<std::mutex> lock(mu);   // a device's stream set is shared by all callers
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+    StreamSet& ss = sets[dev];
     if (ss.dev != dev) {
         for (int k = 0; k < kBatchStreams; ++k) {
             if ((e = cudaStreamCreateWithFlags(&ss.s[k], cudaStreamNonBlocking)) != cudaSuccess) return e;
