@@ -125,13 +125,18 @@ int zero_all_gather(const float* w_shard, float* w_full, int64_t n_shard, void* 
 // Returns an NCCL result (0 = success); *cuda_err receives launch errors.
 int zero_agree_and_select(uint32_t* d_flags, const float* w_old, float* w_scratch, int64_t n_shard, void* comm,
                           cudaStream_t st, cudaError_t* cuda_err) {
-    static LaneBuf lb;
+    static LaneBuf bufs[16];   // per device
     static std::mutex mu;
     uint8_t* lanes = nullptr;
     {
         std::lock_guard<std::mutex> lock(mu);
         int dev = 0;
         cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 16) {
+            *cuda_err = cudaErrorInvalidDevice;
+            return 0;
+        }
+        LaneBuf& lb = bufs[dev];
         if (lb.dev != dev) {
             if ((*cuda_err = cudaMalloc(&lb.p, kLanes)) != cudaSuccess) return 0;
             lb.dev = dev;
