@@ -396,19 +396,14 @@ cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* 
     S.bc1 = a.bc1;
     S.bc2 = a.bc2;
     S.log_target = a.log_target;
-    // Full 512-parameter tiles go through the TMA-pipelined kernel (k1_fast.cu);
-    // the ragged tail (and misaligned buffers) through the generic kernel below.
+    // Whole rounds go through the warp-specialized kernel (k1_ws.cu); the
+    // ragged tail (and misaligned buffers, or a fallback count request) through
+    // the generic kernel below.
     int64_t done = 0;
     if (!fallbacks) {
-        // COAT_K1=v2 selects the previous (per-warp) kernel, for A/B measurement
-        static const bool use_v2 = [] {
-            const char* s = getenv("COAT_K1");
-            return s && s[0] == 'v' && s[1] == '2';
-        }();
-        const int64_t unit = use_v2 ? kTile : k1_ws_round_params();
+        const int64_t unit = k1_ws_round_params();
         const int64_t nfull = n / unit;
-        const cudaError_t e = use_v2 ? launch_k1_fast(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream)
-                                     : launch_k1_ws(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream);
+        const cudaError_t e = launch_k1_ws(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream);
         if (e == cudaSuccess) done = nfull * unit;
         else if (e != cudaErrorNotSupported) return e;
     }
