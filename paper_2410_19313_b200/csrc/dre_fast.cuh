@@ -221,11 +221,15 @@ static __device__ __noinline__ PackParams pack_prepare_fast(uint32_t lo_bits, ui
             if (range > 0x1p200) p.mode = 2;
         } else {
             p.mode = 1;
-            const float r = __fmul_rn(hi, __frcp_rn(p.c));
+            // the SFU evaluation needs a normal RN(1/c): for c outside [2^-100, 2^100]
+            // (e.g. subnormal c of a group of subnormal moments, where 1/c overflows)
+            // go straight to the reference formula (pow of the double quotient)
+            const bool c_ok = p.c >= 0x1p-100f && p.c <= 0x1p100f;
+            const float r = c_ok ? __fmul_rn(hi, __frcp_rn(p.c)) : 1.0f;
             const float e = ex2_approx(__fmul_rn(p.k, lg2_approx(r)));
             const float s_lo = group_scale(__fmul_rn(e, 1.0f - kRelMufu));
             const float s_hi = group_scale(__fmul_rn(e, 1.0f + kRelMufu));
-            if (s_lo == s_hi) {
+            if (c_ok && s_lo == s_hi) {
                 s = s_lo;
             } else {
                 const float am = (float)pow(hid / (double)p.c, (double)p.k);

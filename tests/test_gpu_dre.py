@@ -47,6 +47,7 @@ def special_groups():
     tiny = np.geomspace(1e-38, 1e-36, 128).astype(np.float32); g.append(tiny)   # tiny scales
     big = np.geomspace(1e30, 3e38, 128).astype(np.float32); g.append(big)
     g.append(np.full(128, -0.0, np.float32))                   # all -0 (expand_one(-0) = +0)
+    x = np.geomspace(1e-45, 3e-44, 128).astype(np.float32); g.append(x)   # subnormal c with k > 1
     x = rng(6).standard_normal(128).astype(np.float32); x[1::4] = -0.0; g.append(x)   # -0 among values
     return np.concatenate(g)
 

@@ -1,0 +1,122 @@
+"""GPU: seeded fuzzing of the hot path against the oracle, bit for bit.
+
+Random sizes (ragged, multi-round), random magnitude mixes per 1x128 group
+(normal, log-uniform over many decades, tiny / huge, +-0 runs, constant groups,
+outliers) and random optimizer states; every case is deterministic (seeded).
+K1 (optimizer.cpp:101-114), the MGAQ quantizers (quantize.cpp:89-145) and the
+DRE round trip (expand.cpp:100-141).  Found-bug regressions live in the
+per-component test files; this sweeps the space around them.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CFG = {"beta1": 0.9, "beta2": 0.999, "lr": 1e-3, "weight_decay": 0.1, "eps": 1e-8}
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _host(t):
+    import torch
+    return (t.float() if t.dtype == torch.bfloat16 else t).cpu().numpy()
+
+
+def _mixed(r, n, scale=1.0):
+    """n float32 values, a different distribution per 128-group."""
+    out = np.empty(n, np.float32)
+    for g0 in range(0, n, 128):
+        k = min(128, n - g0)
+        kind = r.integers(0, 8)
+        if kind == 0:
+            x = r.standard_normal(k)
+        elif kind == 1:
+            x = np.exp(r.uniform(-20, 5, k)) * r.choice([-1, 1], k)
+        elif kind == 2:
+            x = np.full(k, r.uniform(-2, 2))
+        elif kind == 3:
+            x = r.standard_normal(k) * 10.0 ** r.uniform(-30, -20)
+        elif kind == 4:
+            x = r.standard_normal(k) * 10.0 ** r.uniform(10, 25)
+        elif kind == 5:
+            x = r.standard_normal(k)
+            x[r.random(k) < 0.5] = 0.0
+            x[r.random(k) < 0.2] = -0.0
+        elif kind == 6:
+            x = r.standard_normal(k)
+            x[r.integers(0, k)] *= 1e4
+        else:
+            x = np.exp(r.uniform(-3, 3, k))
+        out[g0:g0 + k] = (np.asarray(x) * scale).astype(np.float32)
+    return out
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_fuzz_k1_steps(coat, port, case):
+    r = np.random.default_rng(1000 + case)
+    n = int(r.choice([128 * r.integers(1, 40), 1792 * r.integers(1, 200) + r.integers(0, 1792),
+                      int(r.integers(1000, 400_000))]))
+    w = _mixed(r, n, 0.02)
+    m, v = port.make_slot(n)
+    slot = coat.make_slot([n])
+    wg = _dev(w)
+    cfg = dict(CFG, weight_decay=float(r.choice([0.0, 0.1])), lr=float(r.choice([1e-3, 1e-4])))
+    c = coat.AdamWConfig(**cfg)
+    for t in range(int(r.integers(1, 4))):
+        g = _mixed(r, n, float(r.choice([1e-3, 1.0, 1e-6])))
+        if t == 0:   # the first step always compares fully: keep g*g finite
+            g = np.clip(np.nan_to_num(g, posinf=0.0, neginf=0.0), -1e15, 1e15).astype(np.float32)
+        st = port.step(w, g, m, v, t, cfg)
+        assert t > 0 or st == 0, (case, st)
+        if st != 0:   # the reference throws (e.g. g*g overflow -> NonFiniteInput): so must the GPU
+            with pytest.raises(Exception):
+                coat.step(wg, _dev(g), slot, c)
+            return
+        coat.step(wg, _dev(g), slot, c)
+        assert np.array_equal(_host(wg).view(np.uint32), w.view(np.uint32)), (case, t)
+        for st_, ref in ((slot.m, m), (slot.v, v)):
+            assert np.array_equal(_host(st_.quantized.codes), ref["codes"]), (case, t)
+            assert np.array_equal(_host(st_.quantized.scales), ref["scales"]), (case, t)
+            assert np.array_equal(_host(st_.k).view(np.uint32), ref["k"].view(np.uint32)), (case, t)
+            assert np.array_equal(_host(st_.c).view(np.uint32), ref["c"].view(np.uint32)), (case, t)
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_fuzz_mgaq(coat, port, case):
+    import torch
+    r = np.random.default_rng(2000 + case)
+    G = int(r.choice([0, 16, 32, 64, 128]))
+    cols = int(r.choice([16, 48, 128, 384, 4096, 11008])) if G in (0, 16) else int(G * r.integers(1, 40))
+    rows = int(r.integers(1, 300))
+    x = _mixed(r, rows * cols).reshape(rows, cols)
+    bf16 = bool(r.integers(0, 2))
+    if bf16:
+        xt = torch.from_numpy(x).to(torch.bfloat16)
+        x = xt.float().numpy()
+    else:
+        xt = torch.from_numpy(x)
+    if not np.isfinite(x).all():
+        return
+    geo = coat.QuantGeometry.per_group(G) if G else coat.QuantGeometry.per_tensor()
+    q = coat.quantize(xt.cuda(), geo)
+    codes, scales = port.quantize(x, G)
+    assert np.array_equal(_host(q.codes), codes), case
+    assert np.array_equal(_host(q.scales).ravel(), np.asarray(scales).ravel()), case
+
+
+@pytest.mark.parametrize("case", range(20))
+def test_fuzz_dre_round_trip(coat, port, case):
+    r = np.random.default_rng(3000 + case)
+    n = 128 * int(r.integers(1, 3000))
+    x = _mixed(r, n, float(r.choice([1e-6, 1.0, 1e-30])))
+    st = coat.expand_quantize(_dev(x))
+    codes, s, k, c = port.expand_quantize(x)
+    assert np.array_equal(_host(st.quantized.codes), codes), case
+    assert np.array_equal(_host(st.quantized.scales), s), case
+    assert np.array_equal(_host(st.k).view(np.uint32), k.view(np.uint32)), case
+    assert np.array_equal(_host(st.c).view(np.uint32), c.view(np.uint32)), case
+    back = _host(coat.dequantize_contract(st))
+    assert np.array_equal(back.view(np.uint32), port.dequantize_contract(codes, s, k, c).view(np.uint32)), case

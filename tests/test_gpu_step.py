@@ -313,3 +313,29 @@ def test_step_signed_zero_weights_and_grads(coat, port):
         gm, gv = gpu_state(slot)
         assert_state_equal(gm, m, f"m step {t}")
         assert_state_equal(gv, v, f"v step {t}")
+
+
+def test_step_subnormal_moment_groups(coat, port):
+    """Gradients ~1e-21 make v' = (1 - b2) g^2 subnormal; such a group's
+    c = sqrt(lo * hi) is subnormal too, and with k > 1 the expanded maximum
+    must come from pow(hi / (double)c, k) as in the reference (a float
+    RN(1/c) overflows).  Found by tests/test_gpu_fuzz.py."""
+    r = rng(81)
+    n = 128 * 64
+    w0 = (r.standard_normal(n) * 0.02).astype(np.float32)
+    g = (r.standard_normal(n) * 1e-3).astype(np.float32)
+    for q in range(0, 64, 3):   # every third group: subnormal v', mixed with zeros
+        gg = (r.standard_normal(128) * 10.0 ** r.uniform(-22.5, -21)).astype(np.float32)
+        gg[r.random(128) < 0.3] = 0.0
+        g[q * 128:(q + 1) * 128] = gg
+    m, v = port.make_slot(n)
+    w_ref = w0.copy()
+    assert port.step(w_ref, g, m, v, 0, CFG) == 0
+    assert (v["k"] > 1).any() and (v["c"] < 2.0 ** -126).any()   # the case is exercised
+    slot = coat.make_slot([n])
+    w = dev(w0)
+    coat.step(w, dev(g), slot, coat.AdamWConfig(**CFG))
+    assert np.array_equal(host(w).view(np.uint32), w_ref.view(np.uint32))
+    gm, gv = gpu_state(slot)
+    assert_state_equal(gm, m, "m")
+    assert_state_equal(gv, v, "v")
