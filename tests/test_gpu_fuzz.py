@@ -120,3 +120,63 @@ def test_fuzz_dre_round_trip(coat, port, case):
     assert np.array_equal(_host(st.c).view(np.uint32), c.view(np.uint32)), case
     back = _host(coat.dequantize_contract(st))
     assert np.array_equal(back.view(np.uint32), port.dequantize_contract(codes, s, k, c).view(np.uint32)), case
+
+
+def _moment_state(port, r, n, positive):
+    x = _mixed(r, n, float(r.choice([1e-3, 1e-8, 1e-20, 1.0])))
+    if positive:
+        x = np.abs(x)
+    x = np.nan_to_num(x, posinf=0.0, neginf=0.0).astype(np.float32)
+    codes, s, k, c = port.expand_quantize(x)
+    return {"codes": codes, "scales": s, "k": k, "c": c}
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_fuzz_k1_warm_states(coat, port, case):
+    """K1 from random warm states (m, v built by the oracle's expand_quantize of
+    mixed distributions: k spread over [1, 20], tiny and huge scales), random
+    step counters and AdamW settings."""
+    r = np.random.default_rng(4000 + case)
+    n = 128 * int(r.integers(1, 2500))
+    w = _mixed(r, n, float(r.choice([0.02, 1.0, 1e-6])))
+    w = np.clip(np.nan_to_num(w, posinf=0.0, neginf=0.0), -1e30, 1e30).astype(np.float32)
+    m = _moment_state(port, r, n, False)
+    v = _moment_state(port, r, n, True)
+    t0 = int(r.integers(0, 10000))
+    cfg = {"beta1": float(r.choice([0.9, 0.8, 0.95])), "beta2": float(r.choice([0.999, 0.99, 0.95])),
+           "lr": float(r.choice([1e-3, 3e-4, 1e-2])), "weight_decay": float(r.choice([0.0, 0.1, 0.01])),
+           "eps": float(r.choice([1e-8, 1e-6, 1e-12]))}
+    slot = coat.make_slot([n])
+    slot.load_state(m, v, t0)
+    wg = _dev(w)
+    g = _mixed(r, n, float(r.choice([1e-3, 1e-6, 1e-12])))
+    g = np.clip(np.nan_to_num(g, posinf=0.0, neginf=0.0), -1e15, 1e15).astype(np.float32)
+    st = port.step(w, g, m, v, t0, cfg)
+    if st != 0:
+        with pytest.raises(Exception):
+            coat.step(wg, _dev(g), slot, coat.AdamWConfig(**cfg))
+        return
+    coat.step(wg, _dev(g), slot, coat.AdamWConfig(**cfg))
+    assert np.array_equal(_host(wg).view(np.uint32), w.view(np.uint32)), case
+    for st_, ref in ((slot.m, m), (slot.v, v)):
+        assert np.array_equal(_host(st_.quantized.codes), ref["codes"]), case
+        assert np.array_equal(_host(st_.quantized.scales), ref["scales"]), case
+        assert np.array_equal(_host(st_.k).view(np.uint32), ref["k"].view(np.uint32)), case
+        assert np.array_equal(_host(st_.c).view(np.uint32), ref["c"].view(np.uint32)), case
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fuzz_rmsnorm_block(coat, port, case):
+    import torch
+    r = np.random.default_rng(5000 + case)
+    rows, h = int(r.integers(1, 200)), int(16 * r.integers(1, 300))
+    x = _mixed(r, rows * h, float(r.choice([1.0, 1e-3, 30.0]))).reshape(rows, h)
+    x = np.clip(np.nan_to_num(x, posinf=0.0, neginf=0.0), -1e18, 1e18).astype(np.float32)
+    xt = torch.from_numpy(x).to(torch.bfloat16)
+    x = xt.float().numpy()
+    w = (1.0 + 0.2 * r.standard_normal(h)).astype(np.float32)
+    qx, qy, rms, y = coat.rmsnorm_quantize(xt.cuda(), torch.from_numpy(w), eps=1e-6, return_y=True)
+    xc, xs = port.quantize(x, 16)
+    assert np.array_equal(_host(qx.codes), xc) and np.array_equal(_host(qx.scales).ravel(), xs.ravel()), case
+    y_ref = port.rmsnorm(port.dequantize(xc, xs, 16), w, 1e-6)
+    assert np.array_equal(_host(y).view(np.uint32), y_ref.view(np.uint32)), case

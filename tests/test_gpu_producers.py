@@ -23,6 +23,7 @@ def _bf16(a):
 
 
 @pytest.mark.parametrize("rows,h,dtype", [(96, 4096, "bf16"), (33, 512, "fp32"), (8, 11008, "bf16"),
+                                          (89, 272, "bf16"), (7, 16, "fp32"),   # odd groups per row
                                           (8192, 4096, "bf16")])   # the last: cfg2's full rmsnorm input
 def test_rmsnorm_block_bit_exact_vs_oracle(coat, port, rows, h, dtype):
     import torch
@@ -53,7 +54,7 @@ def test_rmsnorm_block_matches_reference_layer_tape(coat, ref):
     assert np.array_equal(_np(qy.codes).reshape(-1), c_q) and np.array_equal(_np(qy.scales), s_q)
 
 
-@pytest.mark.parametrize("rows,cols", [(64, 11008), (40, 512), (8192, 11008)])   # the last: cfg2 full size
+@pytest.mark.parametrize("rows,cols", [(64, 11008), (40, 512), (37, 272), (8192, 11008)])   # the last: cfg2
 def test_silu_mul_block(coat, port, rows, cols):
     import torch
     g = _bf16(port.generate(1, (rows, cols), 0.02, 8.0, 21) * np.float32(2.0))
