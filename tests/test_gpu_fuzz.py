@@ -180,3 +180,30 @@ def test_fuzz_rmsnorm_block(coat, port, case):
     assert np.array_equal(_host(qx.codes), xc) and np.array_equal(_host(qx.scales).ravel(), xs.ravel()), case
     y_ref = port.rmsnorm(port.dequantize(xc, xs, 16), w, 1e-6)
     assert np.array_equal(_host(y).view(np.uint32), y_ref.view(np.uint32)), case
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fuzz_silu_mul_block(coat, port, case):
+    """Random (rows, cols) -- chunk counts that leave the last warp partly
+    filled -- and gate magnitudes that reach silu's large-|x| branch."""
+    import torch
+    r = np.random.default_rng(6000 + case)
+    rows, cols = int(r.integers(1, 200)), int(16 * r.integers(1, 300))
+    g = _mixed(r, rows * cols, float(r.choice([1.0, 30.0, 1e-3]))).reshape(rows, cols)
+    u = _mixed(r, rows * cols, float(r.choice([1.0, 1e-2]))).reshape(rows, cols)
+    g = np.clip(np.nan_to_num(g, posinf=0.0, neginf=0.0), -1e4, 1e4).astype(np.float32)
+    u = np.clip(np.nan_to_num(u, posinf=0.0, neginf=0.0), -1e4, 1e4).astype(np.float32)
+    gt, ut = torch.from_numpy(g).to(torch.bfloat16), torch.from_numpy(u).to(torch.bfloat16)
+    gn, un = gt.float().numpy(), ut.float().numpy()
+    qg, qs, qu, qp, prod = coat.silu_mul_quantize(gt.cuda(), ut.cuda(), return_prod=True)
+    gc, gs = port.quantize(gn, 16)
+    uc, us = port.quantize(un, 16)
+    assert np.array_equal(_host(qg.codes), gc) and np.array_equal(_host(qg.scales).ravel(), gs.ravel()), case
+    assert np.array_equal(_host(qu.codes), uc) and np.array_equal(_host(qu.scales).ravel(), us.ravel()), case
+    s_dq = port.dequantize(_host(qs.codes), _host(qs.scales), 16)
+    p_ref = (s_dq * port.dequantize(uc, us, 16)).astype(np.float32)
+    assert np.array_equal(_host(prod).view(np.uint32), p_ref.view(np.uint32)), case
+    pc, ps = port.quantize(p_ref, 0)
+    assert np.array_equal(_host(qp.codes), pc) and np.array_equal(_host(qp.scales).ravel(), np.asarray(ps).ravel()), case
+    sc, _ = port.quantize(port.silu(port.dequantize(gc, gs, 16)), 16)
+    assert np.count_nonzero(_host(qs.codes) != sc) <= max(2, sc.size // 1000), case
