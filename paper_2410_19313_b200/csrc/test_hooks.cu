@@ -6,6 +6,10 @@
 // pack_prepare_fast side by side; out[i] = 7 floats of each
 // (k, c, s, inv_c, inv_s, mode, bad).  tests/test_gpu_pack_prepare.py checks
 // they agree bit for bit on random and adversarial extrema.
+//
+// coat_test_expf_neg2: expf_neg2 (the paired expf of the SiLU producer) against
+// CUDA's scalar expf(-x) over every float bit pattern in [first, first+count);
+// *mismatches counts the bitwise differences.
 #include <cstdint>
 
 #include "coat_device.cuh"
@@ -39,6 +43,19 @@ __global__ void __launch_bounds__(256) pack_prepare_pair_kernel(const uint32_t* 
     }
 }
 
+__global__ void __launch_bounds__(256) expf_neg2_check_kernel(uint64_t first, uint64_t count, float nz,
+                                                              unsigned long long* mismatches) {
+    unsigned long long bad = 0;
+    for (uint64_t i = 2 * (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x); i < count;
+         i += 2 * uint64_t(gridDim.x) * blockDim.x) {
+        const float x0 = u2f(uint32_t(first + i)), x1 = u2f(uint32_t(first + i + 1));
+        const F2 e = expf_neg2(x0, x1, nz);
+        bad += f2u(e.x) != f2u(expf(-x0));
+        if (i + 1 < count) bad += f2u(e.y) != f2u(expf(-x1));
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
 }  // namespace
 }  // namespace coat
 
@@ -47,5 +64,12 @@ extern "C" int coat_test_pack_prepare(const uint32_t* lo, const uint32_t* hi, in
     if (n <= 0) return 0;
     const unsigned blocks = unsigned((n + 255) / 256);
     coat::pack_prepare_pair_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(lo, hi, n, log_target, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+extern "C" int coat_test_expf_neg2(uint64_t first, uint64_t count, unsigned long long* mismatches, void* stream) {
+    if (count == 0) return 0;
+    coat::expf_neg2_check_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(first, count, -0.0f,
+                                                                                        mismatches);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
