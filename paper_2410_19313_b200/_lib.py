@@ -68,6 +68,7 @@ _SIGS = {
     # internal test hook (csrc/test_hooks.cu), not part of include/coat.h
     "coat_test_pack_prepare": ([_vp, _vp, _i64, C.c_double, _vp, _vp], _int),
     "coat_test_expf_neg2": ([C.c_uint64, C.c_uint64, _vp, _vp], _int),
+    "coat_test_k1_layout": ([], _int),
     "coat_flags_to_status": ([C.c_uint32], _int),
     "coat_device_sm_count": ([], _int),
     "coat_encode_e4m3": ([_vp, _vp, _i64, _vp, _vp], _int),

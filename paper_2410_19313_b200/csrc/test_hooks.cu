@@ -10,6 +10,9 @@
 // coat_test_expf_neg2: expf_neg2 (the paired expf of the SiLU producer) against
 // CUDA's scalar expf(-x) over every float bit pattern in [first, first+count);
 // *mismatches counts the bitwise differences.
+//
+// coat_test_k1_layout: element warps per CTA of the K1 layout this process
+// selected (COAT_K1_EW; tests/test_gpu_k1_layouts.py).
 #include <cstdint>
 
 #include "coat_device.cuh"
@@ -73,3 +76,5 @@ extern "C" int coat_test_expf_neg2(uint64_t first, uint64_t count, unsigned long
                                                                                         mismatches);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
+
+extern "C" int coat_test_k1_layout() { return coat::k1_ws_config(); }

@@ -1,0 +1,33 @@
+"""GPU: K1's alternative CTA layouts are parity-tested like the default.
+
+COAT_K1_EW selects the warp-specialized layout once per process (k1_ws.cu
+k1_ws_config): 7 element warps + 1 helper (default), 6 + 2 helpers (table warp
+and pack warp, 12-group rounds) or 8 + 2 helpers (2 CTAs/SM, 96 registers).
+Each alternative reruns the bit-exact K1 step tests (tests/test_gpu_step.py:
+multi-round and ragged sizes, sparse / zero / extreme groups, NaN codes,
+signed zeros, in-place) and the seeded K1 fuzz cases in a subprocess with
+the variable set."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("ew", ["6", "8"])
+def test_k1_layout_parity(ew):
+    env = dict(os.environ, COAT_K1_EW=ew)
+    probe = subprocess.run([sys.executable, "-c", "from paper_2410_19313_b200 import _lib; "
+                            "print(_lib.lib.coat_test_k1_layout())"],
+                           cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert probe.returncode == 0 and probe.stdout.strip().splitlines()[-1] == ew, probe.stdout + probe.stderr
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          "tests/test_gpu_step.py", "tests/test_gpu_fuzz.py", "-k", "step or k1"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    tail = (out.stdout + out.stderr)[-3000:]
+    assert out.returncode == 0, tail
+    assert " passed" in out.stdout and " failed" not in out.stdout, tail
