@@ -1,4 +1,5 @@
-"""GPU: K1's alternative CTA layouts are parity-tested like the default.
+"""GPU: K1's alternative CTA layouts (and the single-CTA GEMM) are parity-tested
+like the defaults.
 
 COAT_K1_EW selects the warp-specialized layout once per process (k1_ws.cu
 k1_ws_config): 7 element warps + 1 helper (default), 6 + 2 helpers (table warp
@@ -27,6 +28,19 @@ def test_k1_layout_parity(ew):
     assert probe.returncode == 0 and probe.stdout.strip().splitlines()[-1] == ew, probe.stdout + probe.stderr
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                           "tests/test_gpu_step.py", "tests/test_gpu_fuzz.py", "-k", "step or k1"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    tail = (out.stdout + out.stderr)[-3000:]
+    assert out.returncode == 0, tail
+    assert " passed" in out.stdout and " failed" not in out.stdout, tail
+
+
+def test_single_cta_gemm_parity():
+    """COAT_GEMM_CTA=1 forces the single-CTA tcgen05 GEMM (the CTA-pair kernel's
+    A/B baseline, and the product kernel for M <= 128) on every shape: the
+    linear tests pass on it too (cfg4 full size excluded for time)."""
+    env = dict(os.environ, COAT_GEMM_CTA="1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          "tests/test_gpu_linear.py", "-k", "not 8192"],
                          cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     tail = (out.stdout + out.stderr)[-3000:]
     assert out.returncode == 0, tail
