@@ -394,9 +394,9 @@ def main():
             "zero_with_collectives": zero,
             "clocks": sampler.summary(),
             # K1 on the whole rounds + the generic kernel on the n % round tail (if any);
-            # round = 14 groups (COAT_K1_EW=8: 16, =6: 12) of 128 params (k1_ws.cu)
-            "gpu_launches": args.steps * (1 + (1 if n % ({"8": 2048, "6": 1536}.get(
-                os.environ.get("COAT_K1_EW", "")[:1], 1792)) else 0)),
+            # round = 16 groups (COAT_K1_EW=7: 14, =6: 12) of 128 params (k1_ws.cu)
+            "gpu_launches": args.steps * (1 + (1 if n % ({"7": 1792, "6": 1536}.get(
+                os.environ.get("COAT_K1_EW", "")[:1], 2048)) else 0)),
         }
         print(json.dumps(out))
     if ws > 1:

@@ -35,7 +35,7 @@ cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* 
                                   const AdamWScalars& a, uint32_t* flags,
                                   unsigned long long* fallbacks, cudaStream_t stream);
 int k1_ws_config();              // element warps per CTA of the selected layout (COAT_K1_EW)
-int64_t k1_ws_round_params();   // parameters per k1_ws round (1792; COAT_K1_EW=6: 1536, =8: 2048)
+int64_t k1_ws_round_params();   // parameters per k1_ws round (2048; COAT_K1_EW=7: 1792, =6: 1536)
 cudaError_t launch_k1_ws(const float* w_in, float* w_out, const float* g, int64_t nrounds,
                          const MomentStateIn& m_in, const MomentStateIn& v_in, const MomentStateOut& m_out,
                          const MomentStateOut& v_out, const AdamWScalars& a, uint32_t* flags,

@@ -2,8 +2,9 @@
 like the defaults.
 
 COAT_K1_EW selects the warp-specialized layout once per process (k1_ws.cu
-k1_ws_config): 7 element warps + 1 helper (default), 6 + 2 helpers (table warp
-and pack warp, 12-group rounds) or 8 + 2 helpers (2 CTAs/SM, 96 registers).
+k1_ws_config): 8 element warps + 2 helpers (default: table warp and pack warp,
+2 CTAs/SM, 96 registers, 4 stages), 7 + 1 merged helper (3 CTAs/SM, 80
+registers) or 6 + 2 helpers (12-group rounds).
 Each alternative reruns the bit-exact K1 step tests (tests/test_gpu_step.py:
 multi-round and ragged sizes, sparse / zero / extreme groups, NaN codes,
 signed zeros, in-place) and the seeded K1 fuzz cases in a subprocess with
@@ -19,7 +20,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("ew", ["6", "8"])
+@pytest.mark.parametrize("ew", ["6", "7"])
 def test_k1_layout_parity(ew):
     env = dict(os.environ, COAT_K1_EW=ew)
     probe = subprocess.run([sys.executable, "-c", "from paper_2410_19313_b200 import _lib; "
