@@ -32,12 +32,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 P_7B = 6_738_415_616          # Llama-2-7B parameter count
+P_13B = 13_015_864_320        # Llama-2-13B parameter count
 GROUP = 128
 BYTES_PER_PARAM = 16.0 + 40.0 / GROUP   # 16.3125 B/param algorithmic
 CFG = {"beta1": 0.9, "beta2": 0.999, "lr": 1e-3, "weight_decay": 0.1, "eps": 1e-8}
 METRIC = "FP8-DRE AdamW params/sec & HBM GB/s (%roofline) at 1/2/4/8 B200 vs CPU ref"
 WORKLOAD = ("cfg3: Llama-2-7B-shaped optimizer state FP8-DRE AdamW step (E4M3 + DRE, 1x128 "
             "groups, both moments), ZeRO-sharded")
+WORKLOAD_13B = ("cfg5: Llama-2-13B optimizer step (13,015,864,320 params) FP8-DRE AdamW, ZeRO-sharded with "
+                "NCCL gradient reduce-scatter + parameter all-gather")
 
 
 def parse():
@@ -49,6 +52,8 @@ def parse():
     ap.add_argument("--params", type=int, default=P_7B)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="default run: skip the cfg1 / cfg2 / cfg4 measurements added under `extra`")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--mgaq-branches", type=int, default=3,
@@ -56,8 +61,10 @@ def parse():
     ap.add_argument("--mgaq-impl", default="graph", choices=["batch", "graph"],
                     help="batch: coat_quantize_batch (one cooperative launch per layer); graph: the 9 "
                          "per-tensor entry points replayed as a CUDA graph")
-    ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "mgaq", "mgaq-fused", "linear"],
-                    help="adamw7b: BASELINE.json cfg3 (the headline); mgaq: cfg2 activation quantizers")
+    ap.add_argument("--workload", default="adamw7b", choices=["adamw7b", "zero13b", "cfg1", "mgaq", "mgaq-fused", "linear"],
+                    help="adamw7b: BASELINE.json cfg3 (the headline; default run also reports cfg1/cfg2/cfg4 "
+                         "under `extra`); zero13b: cfg5; cfg1: 16 M-param step; mgaq: cfg2 activation "
+                         "quantizers; linear: cfg4")
     return ap.parse_args()
 
 
@@ -192,23 +199,59 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args)
         return
-    if args.workload == "mgaq":
-        run_mgaq(args)
+    single = {"mgaq": run_mgaq, "mgaq-fused": run_mgaq_fused, "linear": run_linear, "cfg1": run_cfg1}
+    if args.workload in single:
+        print(json.dumps(single[args.workload](args)))
         return
-    if args.workload == "mgaq-fused":
-        run_mgaq_fused(args)
-        return
-    if args.workload == "linear":
-        run_linear(args)
-        return
+    run_adamw(args)
+
+
+def _cstate(_lib, mm):
+    return _lib.MomentState(mm["codes"].data_ptr(), mm["scales"].data_ptr(), mm["k"].data_ptr(), mm["c"].data_ptr())
+
+
+def _moment(torch, n, dev):
+    ng = n // GROUP
+    return {"codes": torch.empty(n, dtype=torch.uint8, device=dev),
+            "scales": torch.empty(ng, dtype=torch.int16, device=dev),
+            "k": torch.empty(ng, device=dev), "c": torch.empty(ng, device=dev)}
+
+
+def _fill_synthetic(torch, w, g, gen):
+    """w ~ 0.02 N(0,1); g ~ 1e-3 N(0,1) with 1% outliers x100 (OptimizerLike)."""
+    chunk = 1 << 28
+    for off in range(0, w.numel(), chunk):
+        w[off:off + chunk].normal_(0.0, 0.02, generator=gen)
+    for off in range(0, g.numel(), chunk):
+        gs = g[off:off + chunk]
+        gs.normal_(0.0, 1e-3, generator=gen)
+        gs.mul_(torch.where(torch.rand(gs.shape, device=gs.device, generator=gen) < 0.01, 100.0, 1.0))
+
+
+def _k1_round():
+    # round = 16 groups (COAT_K1_EW=7: 14, =6: 12) of 128 params (k1_ws.cu)
+    return {"7": 1792, "6": 1536}.get(os.environ.get("COAT_K1_EW", "")[:1], 2048)
+
+
+def run_adamw(args):
+    """cfg3 (default) / cfg5 (--workload zero13b): the FP8-DRE AdamW step.
+
+    N = 1: one fused K1 launch per step on the whole state.
+    N > 1: the full ZeRO step per rank -- NCCL reduce-scatter of the fp32
+    gradients -> K1 on the rank's shard -> error-word all-reduce -> NCCL
+    all-gather of the weights -- through the product C-ABI `coat_zero_step`
+    (COAT_BENCH_BACKEND=gloo: the same step from zero.py's torch.distributed
+    collectives, for functional runs of several ranks on one GPU).  `value` is
+    that whole step; K1 alone on the shard is timed beside it (`k1_only`) and
+    is what the roofline describes."""
     import torch
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
     local = local % torch.cuda.device_count()   # (functional runs of N ranks on fewer GPUs)
     torch.cuda.set_device(local)
+    backend = None
     if ws > 1:
-        # NCCL over NVLink; COAT_BENCH_BACKEND=gloo only for functional runs on one GPU
         backend = os.environ.get("COAT_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -217,138 +260,164 @@ def main():
     from paper_2410_19313_b200 import _lib
     L = _lib.lib
 
-    P = args.params
+    P = P_13B if args.workload == "zero13b" else args.params
+    workload = WORKLOAD_13B if args.workload == "zero13b" else WORKLOAD
     if P % (GROUP * ws) != 0:
         raise SystemExit(f"params {P} must be a multiple of {GROUP}*world_size")
     n = P // ws                                     # params owned by this rank
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
-    # ---- device buffers (HBM-resident: w ping-pong, g, E4M3+DRE state ping-pong)
-    w = [torch.empty(n, device=dev), torch.empty(n, device=dev)]
-    g_full = torch.empty(P, device=dev)
-    g = g_full if ws == 1 else torch.empty(n, device=dev)
-    w_full = None if ws == 1 else torch.empty(P, device=dev)
+    # ---- memory plan (180 GB HBM): state ping-pong always; the weights
+    # ping-pong (N = 1) unless that does not fit, then K1 updates w in place
+    free, _tot = torch.cuda.mem_get_info()
+    state_b = 2 * 2 * (n + (n // GROUP) * 10)
+    if ws == 1:
+        need_pp = 12 * P + state_b
+        inplace = need_pp > free * 0.97
+        need = (8 if inplace else 12) * P + state_b
+    else:
+        inplace = False
+        need = 8 * P + 8 * n + state_b
+    if need > free * 0.97:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": f"{workload}: needs {need / 1e9:.1f} GB per rank "
+                                                               f"at N={ws}, {free / 1e9:.1f} GB free",
+                              "n_gpus": ws, "config": {"workload": workload, "params_total": P}}))
+        if ws > 1:
+            dist.destroy_process_group()
+        return
 
-    def moment():
-        ng = n // GROUP
-        return {"codes": torch.empty(n, dtype=torch.uint8, device=dev),
-                "scales": torch.empty(ng, dtype=torch.int16, device=dev),
-                "k": torch.empty(ng, device=dev), "c": torch.empty(ng, device=dev)}
-
-    def cstate(mm):
-        return _lib.MomentState(mm["codes"].data_ptr(), mm["scales"].data_ptr(),
-                                mm["k"].data_ptr(), mm["c"].data_ptr())
-
-    m = [moment(), moment()]
-    v = [moment(), moment()]
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    chunk = 1 << 28
-    for off in range(0, n, chunk):
-        sl = slice(off, min(n, off + chunk))
-        w[0][sl].normal_(0.0, 0.02, generator=gen)
-    for off in range(0, g_full.numel(), chunk):
-        sl = slice(off, min(g_full.numel(), off + chunk))
-        gs = g_full[sl]
-        gs.normal_(0.0, 1e-3, generator=gen)
-        gs.mul_(torch.where(torch.rand(gs.shape, device=dev, generator=gen) < 0.01, 100.0, 1.0))
+    if ws == 1:
+        w0 = torch.empty(n, device=dev)
+        w = [w0, w0 if inplace else torch.empty(n, device=dev)]
+        g = torch.empty(n, device=dev)
+        _fill_synthetic(torch, w0, g, gen)
+        w_full = g_full = g_shard = w_scratch = None
+    else:
+        w_full = torch.empty(P, device=dev)
+        g_full = torch.empty(P, device=dev)
+        g_shard = torch.empty(n, device=dev)
+        w_scratch = torch.empty(n, device=dev)
+        _fill_synthetic(torch, w_full, g_full, gen)
+        # identical weights on every rank (the replicated model), rank-specific gradients
+        dist.broadcast(w_full, 0)
+        w = None
+        g = g_shard
+    m = [_moment(torch, n, dev), _moment(torch, n, dev)]
+    v = [_moment(torch, n, dev), _moment(torch, n, dev)]
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     cfg = _lib.AdamWConfigC(**CFG)
-    st = L.coat_make_slot(n, GROUP, cstate(m[0]), cstate(v[0]), stream.cuda_stream)
+    st = L.coat_make_slot(n, GROUP, _cstate(_lib, m[0]), _cstate(_lib, v[0]), stream.cuda_stream)
     assert st == 0, L.coat_last_error()
+
+    comm = None
+    if ws > 1 and backend == "nccl":
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (C.c_uint8 * 128)()
+            assert L.coat_nccl_unique_id(buf) == 0, L.coat_last_error()
+            uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        uid = uid.to(dev)
+        dist.broadcast(uid, 0)
+        uid_c = (C.c_uint8 * 128)(*uid.cpu().tolist())
+        comm = C.c_void_p()
+        assert L.coat_nccl_comm_init(C.byref(comm), ws, uid_c, rank) == 0, L.coat_last_error()
 
     cur = [0]
     t_step = [0]
-    ev_k = []
 
     def k1(record=None):
+        """K1 alone on this rank's parameters (N > 1: its shard of w_full -> w_scratch)."""
         i = cur[0]
         t_step[0] += 1
+        if ws == 1:
+            w_in, w_out = w[i], w[1 - i]
+        else:
+            w_in, w_out = w_full[rank * n:(rank + 1) * n], w_scratch
         if record is not None:
             record[0].record(stream)
-        s = L.coat_adamw_dre_step(w[i].data_ptr(), w[1 - i].data_ptr(), g.data_ptr(), n, GROUP,
-                                  cstate(m[i]), cstate(v[i]), cstate(m[1 - i]), cstate(v[1 - i]),
-                                  C.byref(cfg), t_step[0], flags.data_ptr(), stream.cuda_stream)
+        s = L.coat_adamw_dre_step(w_in.data_ptr(), w_out.data_ptr(), g.data_ptr(), n, GROUP,
+                                  _cstate(_lib, m[i]), _cstate(_lib, v[i]), _cstate(_lib, m[1 - i]),
+                                  _cstate(_lib, v[1 - i]), C.byref(cfg), t_step[0], flags.data_ptr(),
+                                  stream.cuda_stream)
         if record is not None:
             record[1].record(stream)
         if s != 0:
             raise RuntimeError(L.coat_last_error())
         cur[0] = 1 - i
 
-    flag_bits = torch.zeros(5, dtype=torch.int32, device=dev)
-
-    def step(record=None):
-        """The sharded optimizer step: K1 on this rank's shard of
-        the state, plus (N > 1) the all-reduce of the 5-bit error word every
-        rank needs for the reference's commit semantics (zero.py).  The shards
-        are independent units: no data-path collective."""
-        k1(record)
-        if ws > 1:
-            dist.all_reduce(flag_bits, op=dist.ReduceOp.MAX)
-
     def zero_step():
-        """The full ZeRO step around it: gradient reduce-scatter (fp32, sum) ->
-        K1 on the shard -> parameter all-gather (zero.py ZeroAdamW)."""
-        dist.reduce_scatter_tensor(g, g_full)
-        step()
-        dist.all_gather_into_tensor(w_full, w[cur[0]])
+        """The full ZeRO step: reduce-scatter -> K1 -> error-word
+        agreement -> all-gather."""
+        i = cur[0]
+        t_step[0] += 1
+        if comm is not None:
+            s = L.coat_zero_step(w_full.data_ptr(), g_full.data_ptr(), P, GROUP, _cstate(_lib, m[i]),
+                                 _cstate(_lib, v[i]), _cstate(_lib, m[1 - i]), _cstate(_lib, v[1 - i]),
+                                 C.byref(cfg), t_step[0], g_shard.data_ptr(), w_scratch.data_ptr(),
+                                 flags.data_ptr(), comm, rank, ws, stream.cuda_stream)
+            if s != 0:
+                raise RuntimeError(L.coat_last_error())
+            cur[0] = 1 - i
+        else:   # gloo (functional): zero.py's collectives around the same kernel
+            from paper_2410_19313_b200.zero import all_gather_params, reduce_scatter_grads
+            reduce_scatter_grads(g_full, g_shard)
+            t_step[0] -= 1
+            k1()
+            bits = flags.cpu()
+            dist.all_reduce(bits, op=dist.ReduceOp.MAX)
+            all_gather_params(w_full, w_scratch)
 
-    if ws > 1:
-        dist.reduce_scatter_tensor(g, g_full)   # this rank's gradient shard (sum over ranks)
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
-    torch.cuda.synchronize()
-    with sampler:
-        start.record(stream)
-        for i in range(args.steps):
-            step(evs[i])
-        end.record(stream)
+    def timed(fn, steps, record=False):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)] if record else None
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        with sampler:
+            start.record(stream)
+            for i in range(steps):
+                fn(evs[i]) if record else fn()
+            end.record(stream)
+            torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        ms = start.elapsed_time(end) / steps
+        k_ms = sum(a.elapsed_time(b) for a, b in evs) / steps if record else ms
+        t = torch.tensor([ms, k_ms], device=dev)
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)   # max over ranks
+        return float(t[0]), float(t[1]), sampler.summary()
+
+    # ---- K1 alone (N = 1: this IS the step); CUDA events around every launch
     if ws > 1:
-        dist.barrier()
-    ms = start.elapsed_time(end) / args.steps
-    k_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
-    t = torch.tensor([ms, k_ms], device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, k_ms = float(t[0]), float(t[1])
+        zero_step()     # this rank's gradient shard for the K1-only loop (sum over ranks)
+    for _ in range(args.warmup):
+        k1()
+    ms_k1, k_ms, clocks_k1 = timed(k1, args.steps, record=True)
     fl = int(flags.item())
     assert fl == 0, f"device flags 0x{fl:x}"
 
-    # ---- N > 1: the same steps with the ZeRO collectives around them, reported beside
-    zero = None
+    # ---- N > 1: the whole ZeRO step is the headline
+    ms, clocks = ms_k1, clocks_k1
     if ws > 1:
-        for _ in range(2):
+        for _ in range(max(2, args.warmup)):
             zero_step()
-        torch.cuda.synchronize()
-        dist.barrier()
-        z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        z0.record(stream)
-        for _ in range(args.steps):
-            zero_step()
-        z1.record(stream)
-        torch.cuda.synchronize()
-        dist.barrier()
-        zt = torch.tensor([z0.elapsed_time(z1) / args.steps], device=dev)
-        dist.all_reduce(zt, op=dist.ReduceOp.MAX)
-        zms = float(zt[0])
-        zero = {"ms_per_step": zms, "value": P / (zms * 1e-3), "unit": "params/s",
-                "collectives": f"{dist.get_backend()} reduce_scatter(g fp32, sum) + all_gather(w fp32) "
-                               "around each step",
-                "bytes_per_rank_per_step": int(2 * 4 * P * (ws - 1) / ws)}
+        ms, _, clocks = timed(zero_step, args.steps)
+        assert int(flags.item()) == 0
 
     # ---- end to end through the C-ABI with HOST buffers (pinned), state in HBM
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, L, _lib, n, w, g, m, v, cur, t_step, cfg, cstate, flags, stream, dev, ws)
+        try:
+            e2e = run_e2e(args, L, _lib, P, n, ws, rank, w, g, w_full, g_full, g_shard, w_scratch, m, v, cur,
+                          t_step, cfg, flags, comm, stream, dev, inplace)
+        except Exception as ex:   # pinned-memory limits etc.: report, keep the device numbers
+            e2e = {"error": repr(ex)[:300]}
 
     # ---- roofline of K1 (algorithmic bytes / measured kernel duration)
     peak, peak_kind = measured_peaks()
@@ -367,65 +436,117 @@ def main():
         r1 = reference_step_throughput(1 << 22, 2, 0, 1)
         cpu["value_1_thread"] = r1["value"]
 
+    tail = 1 if n % _k1_round() else 0
+    per_step_launches = (1 + tail) if ws == 1 else ((3 + tail) if comm is not None else (1 + tail))
+    out = None
     if rank == 0:
-        value = P / (ms * 1e-3)
         out = {
-            "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": ws,
+            "metric": METRIC, "value": P / (ms * 1e-3), "unit": "params/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "params_total": P, "params_per_rank": n,
-                       "group": GROUP, "parallelism": f"zero-dp{ws}" + ("" if ws == 1 else
-                                                                         " (state shards, no data-path collective)"),
+            "config": {"workload": workload, "params_total": P, "params_per_rank": n,
+                       "group": GROUP, "parallelism": f"zero-dp{ws}",
                        "state": "E4M3 codes + BF16 scale + fp32 (k, c) per 1x128 group, m and v",
+                       "weights": "updated in place (ping-pong does not fit)" if inplace else "ping-pong",
                        "l2": f"inputs {BYTES_PER_PARAM * n / 1e9:.1f} GB per rank >> 126 MB L2 "
                              "(no flush needed)",
-                       "collectives": "none (N=1)" if ws == 1 else
-                                      "all_reduce of the 5-bit error word per step; the ZeRO "
-                                      "reduce-scatter/all-gather are timed separately (zero_with_collectives)"},
+                       "step": "one fused K1 launch" if ws == 1 else
+                               ("coat_zero_step: NCCL reduce_scatter(g fp32, sum) -> K1 on the shard -> "
+                                "error-word all_reduce -> NCCL all_gather(w fp32)" if comm is not None else
+                                f"{backend}: zero.py reduce_scatter -> K1 -> flag all_reduce -> all_gather "
+                                "(functional run)"),
+                       "collective_bytes_per_rank_per_step": int(2 * 4 * P * (ws - 1) / ws)},
             "kernel_ms": k_ms,
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "frac_of_nominal_8000": achieved / 8000.0,
-                         "algorithmic_bytes_per_param": BYTES_PER_PARAM},
+                         "algorithmic_bytes_per_param": BYTES_PER_PARAM, "kernel": "k1_ws_kernel (K1)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "zero_with_collectives": zero,
-            "clocks": sampler.summary(),
-            # K1 on the whole rounds + the generic kernel on the n % round tail (if any);
-            # round = 16 groups (COAT_K1_EW=7: 14, =6: 12) of 128 params (k1_ws.cu)
-            "gpu_launches": args.steps * (1 + (1 if n % ({"7": 1792, "6": 1536}.get(
-                os.environ.get("COAT_K1_EW", "")[:1], 2048)) else 0)),
+            "clocks": clocks,
+            "gpu_launches": args.steps * per_step_launches,
         }
-        print(json.dumps(out))
+        if ws > 1:
+            out["k1_only"] = {"ms_per_step": ms_k1, "kernel_ms": k_ms, "value": P / (ms_k1 * 1e-3),
+                              "unit": "params/s", "clocks": clocks_k1,
+                              "note": "K1 on every rank's shard, no collectives (max over ranks)"}
+    if comm is not None:
+        torch.cuda.synchronize()
+        L.coat_nccl_comm_destroy(comm)
     if ws > 1:
         dist.destroy_process_group()
+    if rank != 0:
+        return
+    # ---- the other BASELINE configurations, each with its own roofline and clocks
+    if ws == 1 and args.workload == "adamw7b" and not args.no_extra:
+        del w, g, m, v
+        torch.cuda.empty_cache()
+        extra = {}
+        for key, fn in (("cfg1", run_cfg1), ("cfg2", run_mgaq), ("cfg4", run_linear)):
+            try:
+                extra[key] = fn(args, extra_mode=True)
+            except Exception as ex:
+                extra[key] = {"error": repr(ex)[:300]}
+            torch.cuda.empty_cache()
+        out["extra"] = extra
+    print(json.dumps(out))
 
 
-def run_e2e(args, L, _lib, n, w, g, m, v, cur, t_step, cfg, cstate, flags, stream, dev, ws):
+def run_e2e(args, L, _lib, P, n, ws, rank, w, g, w_full, g_full, g_shard, w_scratch, m, v, cur, t_step, cfg,
+            flags, comm, stream, dev, inplace):
+    """The same metric through the product C-ABI with HOST buffers (pinned),
+    host<->device copies inside the timed region.
+    N = 1: coat_adamw_dre_step_host streams w, g in (8 B/param) and w out
+           (4 B/param), 3-stream chunked, the state resident in HBM.
+    N > 1: per rank, H2D of its full gradient (4 B/param of the model) and of
+           its weight shard, coat_zero_step, D2H of its updated weight shard."""
+    import psutil
     import torch
-    # pinned host copies of this rank's w and g (the reference's Tensors live in host memory)
-    w_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    g_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    w_h.copy_(w[cur[0]])
-    g_h.copy_(g[:n])
+    import torch.distributed as dist
+    host_need = (8 * n) if ws == 1 else (4 * P + 4 * n)
+    if psutil.virtual_memory().available < 1.3 * host_need * ws:
+        return {"error": f"needs {host_need * ws / 1e9:.0f} GB of pinned host memory over the ranks, "
+                         f"{psutil.virtual_memory().available / 1e9:.0f} GB available"}
+    if ws == 1:
+        w_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        g_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        w_h.copy_(w[cur[0]])
+        g_h.copy_(g)
+    else:
+        w_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        g_h = torch.empty(P, dtype=torch.float32, pin_memory=True)
+        w_h.copy_(w_full[rank * n:(rank + 1) * n])
+        g_h.copy_(g_full)
     torch.cuda.synchronize()
 
     def one():
         i = cur[0]
         t_step[0] += 1
-        s = L.coat_adamw_dre_step_host(w_h.data_ptr(), w_h.data_ptr(), g_h.data_ptr(), n, GROUP,
-                                       cstate(m[i]), cstate(v[i]), cstate(m[1 - i]),
-                                       cstate(v[1 - i]), C.byref(cfg), t_step[0], flags.data_ptr(),
-                                       0, stream.cuda_stream)
+        if ws == 1:
+            s = L.coat_adamw_dre_step_host(w_h.data_ptr(), w_h.data_ptr(), g_h.data_ptr(), n, GROUP,
+                                           _cstate(_lib, m[i]), _cstate(_lib, v[i]), _cstate(_lib, m[1 - i]),
+                                           _cstate(_lib, v[1 - i]), C.byref(cfg), t_step[0], flags.data_ptr(),
+                                           0, stream.cuda_stream)
+        else:
+            shard = w_full[rank * n:(rank + 1) * n]
+            g_full.copy_(g_h, non_blocking=True)
+            shard.copy_(w_h, non_blocking=True)
+            s = L.coat_zero_step(w_full.data_ptr(), g_full.data_ptr(), P, GROUP, _cstate(_lib, m[i]),
+                                 _cstate(_lib, v[i]), _cstate(_lib, m[1 - i]), _cstate(_lib, v[1 - i]),
+                                 C.byref(cfg), t_step[0], g_shard.data_ptr(), w_scratch.data_ptr(),
+                                 flags.data_ptr(), comm, rank, ws, stream.cuda_stream) if comm is not None else -1
+            w_h.copy_(shard, non_blocking=True)
         if s != 0:
-            raise RuntimeError(L.coat_last_error())
+            raise RuntimeError(L.coat_last_error() if s > 0 else "e2e at N>1 needs the NCCL backend")
         cur[0] = 1 - i
 
     one()
     torch.cuda.synchronize()
     K = max(1, args.e2e_steps)
+    if ws > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
@@ -437,12 +558,94 @@ def run_e2e(args, L, _lib, n, w, g, m, v, cur, t_step, cfg, cstate, flags, strea
     wall = (time.perf_counter() - t0) / K
     t = torch.tensor([ms], device=dev)
     if ws > 1:
-        import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
-    return {"value": n * ws / (ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 8 * n,
+    if ws == 1:
+        return {"value": n / (ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 4 * n, "ms_per_step": ms, "wall_s_per_step": wall, "steps": K,
+                "path": "coat_adamw_dre_step_host: pinned host w,g -> 3-stream chunked H2D / K1 / D2H"}
+    return {"value": P / (ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 4 * P + 4 * n,
             "d2h_bytes_per_step": 4 * n, "ms_per_step": ms, "wall_s_per_step": wall, "steps": K,
-            "path": "coat_adamw_dre_step_host: pinned host w,g -> 3-stream chunked H2D / K1 / D2H"}
+            "per_rank": True,
+            "path": "per rank: pinned H2D of its full fp32 gradient and its weight shard -> coat_zero_step "
+                    "(NCCL RS -> K1 -> AG) -> D2H of its updated shard"}
+
+
+# ------------------------------------------------------ cfg1: 16 M-param K1 ----
+def run_cfg1(args, extra_mode=False):
+    """BASELINE.json configs[0]: the FP8-DRE AdamW step on a 16 M-param fp32
+    tensor (2^24 params, 273.7 MB of algorithmic traffic per step > the 126 MB
+    L2 -- no flush needed).  Launch-bound at this size: the steps are replayed
+    as CUDA graphs of 50 launches for >= 1 s under the clock sampler."""
+    import torch
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    n = 1 << 24
+    gen = torch.Generator(device=dev).manual_seed(16)
+    w = [torch.empty(n, device=dev), torch.empty(n, device=dev)]
+    g = torch.empty(n, device=dev)
+    _fill_synthetic(torch, w[0], g, gen)
+    m = [_moment(torch, n, dev), _moment(torch, n, dev)]
+    v = [_moment(torch, n, dev), _moment(torch, n, dev)]
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    cfg = _lib.AdamWConfigC(**CFG)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    per_graph = 50
+    with torch.cuda.stream(side):
+        s = side.cuda_stream
+        assert L.coat_make_slot(n, GROUP, _cstate(_lib, m[0]), _cstate(_lib, v[0]), s) == 0
+
+        def launch(t):
+            i = (t - 1) % 2
+            assert L.coat_adamw_dre_step(w[i].data_ptr(), w[1 - i].data_ptr(), g.data_ptr(), n, GROUP,
+                                         _cstate(_lib, m[i]), _cstate(_lib, v[i]), _cstate(_lib, m[1 - i]),
+                                         _cstate(_lib, v[1 - i]), C.byref(cfg), t, flags.data_ptr(), s) == 0
+        for t in range(1, 11):
+            launch(t)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            for t in range(11, 11 + per_graph):
+                launch(t)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        # >= 1 s of replays
+        t0 = time.perf_counter()
+        graph.replay()
+        torch.cuda.synchronize()
+        reps = max(3, int(1.0 / max(time.perf_counter() - t0, 1e-6)) + 1)
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(0)
+        with sampler:
+            start.record(side)
+            for _ in range(reps):
+                graph.replay()
+            end.record(side)
+            torch.cuda.synchronize()
+    assert int(flags.item()) == 0
+    ms = start.elapsed_time(end) / (reps * per_graph)
+    peak, kind = measured_peaks()
+    gbs = BYTES_PER_PARAM * n / (ms * 1e-3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        r = reference_step_throughput(n, 2, 1, os.cpu_count() or 1)
+        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    return {
+        "metric": "FP8-DRE AdamW step, 16 M params (cfg1): params/s & HBM GB/s",
+        "value": n / (ms * 1e-3), "unit": "params/s", "us_per_step": ms * 1e3, "steps": reps * per_graph,
+        "higher_is_better": True, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg1: FP8 AdamW + DRE step, 16,777,216 fp32 params, 1x128 groups",
+                   "params": n, "l2": "273.7 MB algorithmic per step > 126 MB L2 (no flush)",
+                   "impl": f"coat_adamw_dre_step replayed as CUDA graphs of {per_graph} launches"},
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                     "traffic": None, "peak_kind": kind, "ideal_us": BYTES_PER_PARAM * n / (peak * 1e9) * 1e6},
+        "cpu_baseline": cpu, "clocks": sampler.summary(), "gpu_launches": reps * per_graph,
+    }
 
 
 # ------------------------------------------------ cfg2: MGAQ quantizers ----
@@ -453,7 +656,52 @@ MGAQ_TENSORS = [  # (name, rows, cols, granularity) -- flow.cpp:546-612 call sit
 ]
 
 
-def run_mgaq(args):
+def _reps_for(fn, min_s, at_least):
+    """Replays of fn() to cover >= min_s seconds (one timed probe)."""
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fn()
+    torch.cuda.synchronize()
+    return max(at_least, int(min_s / max(time.perf_counter() - t0, 1e-6)) + 1)
+
+
+def _threaded(jobs, threads):
+    """Run independent ctypes jobs (they release the GIL) on `threads` host threads; wall seconds."""
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda f: f(), jobs))
+    return time.perf_counter() - t0
+
+
+def mgaq_cpu_baseline(rows=256):
+    """The unmodified reference's `quantize` (quantize.cpp:89-145; oracle/_ref)
+    on a bounded sample of the cfg2 layer: the first `rows` token rows of each
+    of the nine records, each record's quantization an independent job, all
+    host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    from pyoracle import Oracle, available
+    kind = "reference" if available("reference") else "port"
+    o = Oracle(kind)
+    r = np.random.default_rng(7)
+    jobs, elems = [], 0
+    for name, _r, c, G in MGAQ_TENSORS:
+        x = (r.standard_normal((rows, c)) * 2).astype(np.float32)
+        x[::100] *= 50
+        x = (x.view(np.uint32) & 0xFFFF0000).view(np.float32)   # bf16-valued, as the device input
+        jobs.append(lambda x=x, G=G: o.quantize(x, G))
+        elems += rows * c
+    threads = os.cpu_count() or 1
+    _threaded(jobs, threads)   # warm
+    dt = _threaded(jobs, threads)
+    return {"value": elems / dt, "unit": "elements/s", "cores": min(threads, len(jobs)), "kind": kind,
+            "sample": f"first {rows} token rows of each of the 9 cfg2 records ({elems} elements), one "
+                      f"quantize per record, records in parallel on {min(threads, len(jobs))} threads"}
+
+
+def run_mgaq(args, extra_mode=False):
     """BASELINE.json cfg2: quantize one Llama-2-7B decoder layer's saved
     activations (B=4, S=2048, H=4096, I=11008; bf16 in): per-group 1x16 for the
     non-linear inputs, per-tensor with two-stage Group Scaling amax (stage-1
@@ -565,15 +813,16 @@ def run_mgaq(args):
            for name, *_ in MGAQ_TENSORS}
     per = {name: 0.0 for name, *_ in MGAQ_TENSORS}
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = _reps_for(run_once, 1.0, args.steps)   # >= 1 s under the clock sampler
     sampler = ClockSampler(0)
     with sampler:
         start.record(stream)
-        for _ in range(args.steps):
+        for _ in range(reps):
             run_once()
         end.record(stream)
         torch.cuda.synchronize()
-    ms = start.elapsed_time(end) / args.steps
-    launches = launches_per_step * args.steps
+    ms = start.elapsed_time(end) / reps
+    launches = launches_per_step * reps
     # per-tensor timing from one extra instrumented (eager) pass
     step(evs)
     torch.cuda.synchronize()
@@ -581,9 +830,15 @@ def run_mgaq(args):
         per[name] = evs[name][0].elapsed_time(evs[name][1])
     peak, kind = measured_peaks()
     gbs = alg_bytes / (ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "mgaq_dram_bytes.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f)["dram_bytes_per_layer"]
+    cpu = None if args.no_cpu_baseline else mgaq_cpu_baseline()
     out = {
         "metric": "MGAQ activation quantization, Llama-2-7B layer (cfg2): elements/s & HBM GB/s",
-        "value": nel / (ms * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+        "value": nel / (ms * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": reps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
         "config": {"workload": "cfg2: MGAQ of one Llama-2-7B decoder layer, B4 x S2048 x H4096, I=11008",
@@ -595,14 +850,16 @@ def run_mgaq(args):
                    "l2": "per-tensor inputs of 64-180 MB: stage-2 re-read partly L2-resident"},
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "frac_of_nominal_8000": gbs / 8000.0,
-                     "traffic": None, "peak_kind": kind, "algorithmic_bytes": alg_bytes},
-        "per_tensor_ms": per, "clocks": sampler.summary(), "gpu_launches": launches,
+                     "traffic": traffic, "peak_kind": kind, "algorithmic_bytes": alg_bytes,
+                     "traffic_source": "ncu dram__bytes_read+write summed over the layer's kernels "
+                                       "(profiles/mgaq_dram_bytes.json)"},
+        "per_tensor_ms": per, "cpu_baseline": cpu, "clocks": sampler.summary(), "gpu_launches": launches,
     }
-    print(json.dumps(out))
+    return out
 
 
 # ------------------------------------- cfg2 with the producers fused (a17) ----
-def run_mgaq_fused(args):
+def run_mgaq_fused(args, extra_mode=False):
     """cfg2's nine MGAQ records of a Llama-2-7B layer produced by the fused
     producer blocks (flow.cpp:546-612): coat_rmsnorm_quant x2 (rmsnorm1.in +
     qkv.in, rmsnorm2.in + upgate.in), coat_silu_mul_quant (silu.in,
@@ -675,14 +932,15 @@ def run_mgaq_fused(args):
             per_step = step()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = _reps_for(graph.replay, 1.0, args.steps)
     sampler = ClockSampler(0)
     with sampler:
         start.record(stream)
-        for _ in range(args.steps):
+        for _ in range(reps):
             graph.replay()
         end.record(stream)
         torch.cuda.synchronize()
-    ms = start.elapsed_time(end) / args.steps
+    ms = start.elapsed_time(end) / reps
     assert int(flags.item()) == 0
     elems = 5 * N * H + 4 * N * I                  # the nine records (same elements as cfg2)
     inputs = 2 * (4 * N * H + 2 * N * I)           # x, r1, attn, gate, up (bf16) read once
@@ -693,7 +951,7 @@ def run_mgaq_fused(args):
     gbs = alg / (ms * 1e-3) / 1e9
     out = {
         "metric": "MGAQ + fused producers, Llama-2-7B layer (cfg2 records): elements/s & HBM GB/s",
-        "value": elems / (ms * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+        "value": elems / (ms * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": reps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
         "config": {"workload": "cfg2 records via fused producers: rmsnorm_quant x2, silu_mul_quant, attn.out per-tensor",
@@ -703,13 +961,56 @@ def run_mgaq_fused(args):
                      "frac_of_nominal_8000": gbs / 8000.0,
                      "traffic": None, "peak_kind": kind, "algorithmic_bytes": alg,
                      "basis": "bf16 inputs once + all codes and scales written"},
-        "clocks": sampler.summary(), "gpu_launches": per_step * args.steps,
+        "clocks": sampler.summary(), "gpu_launches": per_step * reps,
     }
-    print(json.dumps(out))
+    return out
 
 
 # ----------------------------------------------- cfg4: FP8 linear fwd+bwd ----
-def run_linear(args):
+def fp8_burst_peak_tflops():
+    """cuBLASLt FP8 (E4M3 x E4M3 -> bf16, torch._scaled_mm) at 8192^3, best of 10
+    back-to-back timings -- the measured FP8 denominator of cfg4's roofline."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, device="cuda").to(torch.float8_e4m3fn)
+    b = torch.randn(n, n, device="cuda").to(torch.float8_e4m3fn).t()
+    one = torch.ones((), device="cuda")
+    for _ in range(3):
+        torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+    best = 1e9
+    for _ in range(10):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(5):
+            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        s1.record()
+        torch.cuda.synchronize()
+        best = min(best, s0.elapsed_time(s1) / 5)
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def linear_cpu_baseline(rows=16):
+    """The reference's linear (flow.cpp:21-33: sequential fp32 accumulation in
+    p order; restated in the oracle port -- the reference's matmul is in an
+    anonymous namespace) on a bounded sample: `rows` token rows per host
+    thread of the cfg4 forward, rows sharded over all host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    from pyoracle import Oracle
+    o = Oracle("port")
+    K, N = 5120, 13824
+    r = np.random.default_rng(11)
+    w = (r.standard_normal((K, N)) / K ** 0.5).astype(np.float32)
+    threads = os.cpu_count() or 1
+    xs = [(r.standard_normal((rows, K))).astype(np.float32) for _ in range(threads)]
+    dt = _threaded([lambda x=x: o.matmul(x, w) for x in xs], threads)
+    flop = 2.0 * rows * threads * K * N
+    return {"value": flop / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"{rows * threads} token rows of the cfg4 forward (x[rows,5120] . W[5120,13824]), "
+                      f"{rows} rows per thread on {threads} threads"}
+
+
+def run_linear(args, extra_mode=False):
     """BASELINE.json cfg4: per-tensor FP8 E4M3 linear forward + backward with
     Group Scaling amax, Llama-2-13B MLP shape (8192 tokens x 5120 x 13824).
     One step = Group-Scaling quantize of x (bf16) and W (fp32), fwd GEMM
@@ -766,15 +1067,16 @@ def run_linear(args):
         step()
     torch.cuda.synchronize()
     per = {k: 0.0 for k in names}
+    reps = _reps_for(step, 1.0, args.steps)
     sampler = ClockSampler(0)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with sampler:
         start.record(st)
-        for _ in range(args.steps):
+        for _ in range(reps):
             step(rec=True)
             torch.cuda.synchronize()
             for k in names:
-                per[k] += ev[k][0].elapsed_time(ev[k][1]) / args.steps
+                per[k] += ev[k][0].elapsed_time(ev[k][1]) / reps
         end.record(st)
         torch.cuda.synchronize()
     flop = 2.0 * M * N * K
@@ -782,25 +1084,31 @@ def run_linear(args):
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             bf16_peak = float(json.load(f)["bf16_tflops"])
-        kind = "measured bf16 (cuBLAS burst); fp8 peak taken as 2x"
+        bf16_kind = "measured bf16 (MEASURED_PEAKS.json, cuBLAS burst)"
     except Exception:
-        bf16_peak, kind = 1590.0, "fallback"
+        bf16_peak, bf16_kind = 1590.0, "fallback"
+    try:
+        fp8_peak, kind = fp8_burst_peak_tflops(), "measured here: cuBLASLt FP8 _scaled_mm 8192^3 burst"
+    except Exception as ex:
+        fp8_peak, kind = 2 * bf16_peak, f"2x bf16 (FP8 probe failed: {ex!r:.80})"
+    cpu = None if args.no_cpu_baseline else linear_cpu_baseline()
     tf = {k: flop / (per[k] * 1e-3) / 1e12 for k in ("fwd", "dgrad", "wgrad")}
     out = {
         "metric": "Per-tensor FP8 linear fwd+bwd (cfg4), TFLOP/s", "value": 3 * flop / (ms * 1e-3) / 1e12,
-        "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "unit": "TFLOP/s", "n_gpus": 1, "steps": reps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "e4m3 fwd / bf16 bwd, fp32 acc",
         "data": "synthetic",
         "config": {"workload": "cfg4: Llama-2-13B MLP linear, 8192 tokens x 5120 x 13824, per-tensor E4M3",
                    "M": M, "K": K, "N": N},
         "per_phase_ms": per, "tflops": tf,
-        "roofline": {"bound": "tensor", "achieved": tf["fwd"], "peak": 2 * bf16_peak, "unit": "TFLOP/s",
-                     "frac": tf["fwd"] / (2 * bf16_peak), "traffic": None, "peak_kind": kind,
-                     "frac_of_nominal_4500": tf["fwd"] / 4500.0,
-                     "bwd_frac_of_bf16": {"dgrad": tf["dgrad"] / bf16_peak, "wgrad": tf["wgrad"] / bf16_peak}},
-        "clocks": sampler.summary(), "gpu_launches": 9 * args.steps,
+        "roofline": {"bound": "tensor", "achieved": tf["fwd"], "peak": fp8_peak, "unit": "TFLOP/s",
+                     "frac": tf["fwd"] / fp8_peak, "traffic": None, "peak_kind": kind,
+                     "frac_of_nominal_4500": tf["fwd"] / 4500.0, "kernel": "gemm_kernel (K4) FP8 forward",
+                     "bwd_frac_of_bf16": {"dgrad": tf["dgrad"] / bf16_peak, "wgrad": tf["wgrad"] / bf16_peak},
+                     "bf16_peak": bf16_peak, "bf16_peak_kind": bf16_kind},
+        "cpu_baseline": cpu, "clocks": sampler.summary(), "gpu_launches": 9 * reps,
     }
-    print(json.dumps(out))
+    return out
 
 
 if __name__ == "__main__":

@@ -225,7 +225,8 @@ coat_status coat_adamw_dre_step_host(const float* w_host_in, float* w_host_out, 
  * fp32 buffers (FlatLayout: every tensor 128-aligned, n_total % (128*nranks) ==
  * 0); this rank owns [rank*n, (rank+1)*n), n = n_total / nranks, and only that
  * shard's state (m_in, v_in -> m_out, v_out as in coat_adamw_dre_step).
- * g_shard, w_scratch: n-float device scratch.  Stream-ordered, no host sync:
+ * g_shard, w_scratch: n-float device scratch (g_shard is also reused for the
+ * error-word lanes once the step has consumed it).  Stream-ordered, no host sync:
  * reduce-scatter (sum) g_full -> g_shard; the fused step on the shard into
  * w_scratch; all-reduce of the error word so *d_flags (zeroed by the caller)
  * is the OR over all ranks; when the step must change nothing

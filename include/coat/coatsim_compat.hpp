@@ -314,6 +314,15 @@ struct DevMoment {
     explicit DevMoment(int64_t npad)
         : codes(size_t(npad)), scales(size_t(npad / 128)), k(size_t(npad / 128)), c(size_t(npad / 128)) {}
     coat_moment_state cs() const { return {codes.p, scales.p, k.p, c.p}; }
+    // device-to-device deep copy (OptimizerSlot is a value type in the reference)
+    std::shared_ptr<DevMoment> clone() const {
+        auto o = std::make_shared<DevMoment>(int64_t(codes.n));
+        cuda(cudaMemcpy(o->codes.p, codes.p, codes.n, cudaMemcpyDeviceToDevice));
+        cuda(cudaMemcpy(o->scales.p, scales.p, 2 * scales.n, cudaMemcpyDeviceToDevice));
+        cuda(cudaMemcpy(o->k.p, k.p, 4 * k.n, cudaMemcpyDeviceToDevice));
+        cuda(cudaMemcpy(o->c.p, c.p, 4 * c.n, cudaMemcpyDeviceToDevice));
+        return o;
+    }
     void upload(const ExpandedQuantState& s) {
         codes.upload(s.quantized.codes.data(), codes.n);
         std::vector<uint16_t> s16(scales.n);
@@ -398,6 +407,9 @@ struct SlotPolicy {
 
 // The state lives in HBM: two buffer sets per moment (ping-pong) so a failed
 // step commits exactly what the reference commits (optimizer.cpp:101-114).
+// OptimizerSlot is a VALUE type as in the reference (optimizer.hpp:48-52):
+// copying a slot deep-copies its device state (both ping-pong sets), so
+// stepping a copy never touches the original's moments.  Moves are cheap.
 struct OptimizerSlot {
     std::vector<int64_t> shape;
     SlotPolicy policy;
@@ -407,6 +419,24 @@ struct OptimizerSlot {
     int cm = 0, cv = 0;
     ExpandedQuantState m() const { return mbuf[cm]->download({npad}); }
     ExpandedQuantState v() const { return vbuf[cv]->download({npad}); }
+
+    OptimizerSlot() = default;
+    OptimizerSlot(OptimizerSlot&&) noexcept = default;
+    OptimizerSlot& operator=(OptimizerSlot&&) noexcept = default;
+    OptimizerSlot(const OptimizerSlot& o)
+        : shape(o.shape), policy(o.policy), step(o.step), npad(o.npad), cm(o.cm), cv(o.cv) {
+        for (int i = 0; i < 2; ++i) {
+            if (o.mbuf[i]) mbuf[i] = o.mbuf[i]->clone();
+            if (o.vbuf[i]) vbuf[i] = o.vbuf[i]->clone();
+        }
+    }
+    OptimizerSlot& operator=(const OptimizerSlot& o) {
+        if (this != &o) {
+            OptimizerSlot tmp(o);
+            *this = std::move(tmp);
+        }
+        return *this;
+    }
 };
 
 inline OptimizerSlot make_slot(const std::vector<int64_t>& shape, const SlotPolicy& policy = {}) {

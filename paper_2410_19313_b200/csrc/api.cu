@@ -374,7 +374,8 @@ coat_status coat_zero_step(float* w_full, const float* g_full, int64_t n_total, 
                                            out_of(v_out), a, d_flags, g_fallback_counter, s));
     if (st != COAT_OK) return st;
     cudaError_t ce = cudaSuccess;
-    st = nccl_status(zero_agree_and_select(d_flags, w_own, w_scratch, n, comm, s, &ce), "ncclAllReduce");
+    st = nccl_status(zero_agree_and_select(d_flags, w_own, w_scratch, n, comm,
+                                           reinterpret_cast<uint8_t*>(g_shard), s, &ce), "ncclAllReduce");
     if (st != COAT_OK) return st;
     if ((st = cuda_status(ce)) != COAT_OK) return st;
     return nccl_status(zero_all_gather(w_scratch, w_full, n, comm, s), "ncclAllGather");

@@ -160,6 +160,6 @@ int nccl_comm_destroy(void* comm);
 int zero_reduce_scatter(const float* g_full, float* g_shard, int64_t n_shard, void* comm, cudaStream_t st);
 int zero_all_gather(const float* w_shard, float* w_full, int64_t n_shard, void* comm, cudaStream_t st);
 int zero_agree_and_select(uint32_t* d_flags, const float* w_old, float* w_scratch, int64_t n_shard, void* comm,
-                          cudaStream_t st, cudaError_t* cuda_err);
+                          uint8_t* lanes, cudaStream_t st, cudaError_t* cuda_err);
 
 }  // namespace coat

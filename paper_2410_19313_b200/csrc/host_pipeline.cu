@@ -13,8 +13,8 @@
 // Three staging slots (w and g, `chunk` fp32 each) let chunk i+1 upload while
 // chunk i computes and chunk i-1 downloads.  Host buffers must be pinned
 // (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous.
-// Chunks are multiples of the fused kernel's round (k1_ws_round_params(): 14
-// groups of 128), so every chunk starts on a 1x128 group boundary, uses the
+// Chunks are multiples of the fused kernel's round (k1_ws_round_params():
+// 16 groups of 128 in the default EW = 8 layout), so every chunk starts on a 1x128 group boundary, uses the
 // state slice of its own groups, and only the last one has a ragged tail.
 #include <cstdint>
 #include <mutex>
@@ -112,7 +112,10 @@ cudaError_t host_pipelined_step(const float* w_host_in, float* w_host_out, const
         const int s = int(i % kSlots);
         const int64_t off = i * chunk;
         const int64_t len = n - off < chunk ? n - off : chunk;
-        if (i >= kSlots) cudaStreamWaitEvent(ws.h2d, ws.down[s], 0);   // slot drained
+        // slot drained -- also for the first kSlots chunks: the previous call's
+        // D2H of this slot may still be in flight on another caller stream
+        // (never-recorded events count as complete)
+        cudaStreamWaitEvent(ws.h2d, ws.down[s], 0);
         cudaMemcpyAsync(ws.w[s], w_host_in + off, sizeof(float) * size_t(len), cudaMemcpyHostToDevice, ws.h2d);
         cudaMemcpyAsync(ws.g[s], g_host + off, sizeof(float) * size_t(len), cudaMemcpyHostToDevice, ws.h2d);
         cudaEventRecord(ws.up[s], ws.h2d);

@@ -265,7 +265,9 @@ void get_moment(Reader& r, int64_t npad, int64_t G, HostMoment& h) {
     }
 }
 
-cudaError_t h2d(const coat_moment_state& st, const HostMoment& h, cudaStream_t s) {
+// BF16 bit patterns of a moment's scales; throws (before anything reaches the
+// device) when a scale is not BF16-valued.
+std::vector<uint16_t> bf16_scales(const HostMoment& h) {
     const size_t ng = h.scales.size();
     std::vector<uint16_t> sb(ng);
     for (size_t i = 0; i < ng; ++i) {
@@ -274,6 +276,11 @@ cudaError_t h2d(const coat_moment_state& st, const HostMoment& h, cudaStream_t s
         if (bits & 0xFFFFu) throw std::invalid_argument("scale is not BF16-valued (BF16-scale policy expected)");
         sb[i] = uint16_t(bits >> 16);
     }
+    return sb;
+}
+
+cudaError_t h2d(const coat_moment_state& st, const HostMoment& h, const std::vector<uint16_t>& sb, cudaStream_t s) {
+    const size_t ng = sb.size();
     cudaError_t e = cudaMemcpyAsync(st.codes, h.codes.data(), h.codes.size(), cudaMemcpyHostToDevice, s);
     if (!e) e = cudaMemcpyAsync(st.scales, sb.data(), ng * 2, cudaMemcpyHostToDevice, s);
     if (!e) e = cudaMemcpyAsync(st.k, h.k.data(), ng * 4, cudaMemcpyHostToDevice, s);
@@ -345,24 +352,30 @@ coat_status load_slot_impl(const char* path, const int64_t* shape, int rank, int
                 return COAT_ERR_INVALID;
             }
         }
-        cfg->beta1 = float(h.at("beta1").num);
-        cfg->beta2 = float(h.at("beta2").num);
-        cfg->lr = float(h.at("lr").num);
-        cfg->weight_decay = float(h.at("weight_decay").num);
-        cfg->eps = float(h.at("eps").num);
-        *step = h.at("step").i;
+        coat_adamw_config c;
+        c.beta1 = float(h.at("beta1").num);
+        c.beta2 = float(h.at("beta2").num);
+        c.lr = float(h.at("lr").num);
+        c.weight_decay = float(h.at("weight_decay").num);
+        c.eps = float(h.at("eps").num);
+        const int64_t st = h.at("step").i;
         int64_t n = 1;
         for (int i = 0; i < rank; ++i) n *= shape[i];
         const int64_t npad = (n + G - 1) / G * G;
         HostMoment hm, hv;
         get_moment(r, npad, G, hm);
         get_moment(r, npad, G, hv);
-        cudaError_t e = h2d(m, hm, s);
-        if (!e) e = h2d(v, hv, s);
+        // all-or-nothing like read_slot: both moments parsed and validated
+        // before the first byte reaches the device or the outputs
+        const std::vector<uint16_t> sm = bf16_scales(hm), sv = bf16_scales(hv);
+        cudaError_t e = h2d(m, hm, sm, s);
+        if (!e) e = h2d(v, hv, sv, s);
         if (e) {
             err = cudaGetErrorString(e);
             return COAT_ERR_CUDA;
         }
+        *cfg = c;
+        *step = st;
     } catch (const std::domain_error& ex) {
         err = ex.what();
         return COAT_ERR_BAD_MAGIC;

@@ -75,11 +75,6 @@ __global__ void lanes_commit_kernel(const uint8_t* lanes, uint32_t* flags, const
         w_scratch[i] = w_old[i];
 }
 
-struct LaneBuf {
-    int dev = -1;
-    uint8_t* p = nullptr;
-};
-
 }  // namespace
 
 bool nccl_available() { return api().ok; }
@@ -122,27 +117,13 @@ int zero_all_gather(const float* w_shard, float* w_full, int64_t n_shard, void* 
 }
 
 // *d_flags := OR over ranks; w_scratch := w_old when nothing may change.
+// `lanes` is kLanes bytes of per-call device scratch (coat_zero_step passes
+// the head of its g_shard, which the fused step has consumed by then in
+// stream order), so concurrent ZeRO steps -- other communicators, other
+// streams on the same device -- never share it.
 // Returns an NCCL result (0 = success); *cuda_err receives launch errors.
 int zero_agree_and_select(uint32_t* d_flags, const float* w_old, float* w_scratch, int64_t n_shard, void* comm,
-                          cudaStream_t st, cudaError_t* cuda_err) {
-    static LaneBuf bufs[16];   // per device
-    static std::mutex mu;
-    uint8_t* lanes = nullptr;
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 0 || dev >= 16) {
-            *cuda_err = cudaErrorInvalidDevice;
-            return 0;
-        }
-        LaneBuf& lb = bufs[dev];
-        if (lb.dev != dev) {
-            if ((*cuda_err = cudaMalloc(&lb.p, kLanes)) != cudaSuccess) return 0;
-            lb.dev = dev;
-        }
-        lanes = lb.p;
-    }
+                          uint8_t* lanes, cudaStream_t st, cudaError_t* cuda_err) {
     flags_to_lanes_kernel<<<1, 32, 0, st>>>(d_flags, lanes);
     if ((*cuda_err = cudaGetLastError()) != cudaSuccess) return 0;
     const ncclResult_t r = api().all_reduce(lanes, lanes, kLanes, ncclUint8, ncclMax, static_cast<ncclComm_t>(comm), st);

@@ -106,12 +106,23 @@ def _world(group) -> tuple[int, int]:
     return 1, 0
 
 
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """gloo has no CUDA reduce-scatter / all-gather-into-tensor: stage CUDA
+    buffers through host memory (functional multi-rank runs on one GPU --
+    tests/test_gpu_zero_multirank.py; NCCL takes the device buffers as is)."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def reduce_scatter_grads(g_full: torch.Tensor, g_shard: torch.Tensor, group=None, grad_op: str = "sum") -> None:
     """g_shard = (sum over ranks of g_full)[this rank's shard]; grad_op="avg" divides by world size."""
     ws, _ = _world(group)
     if ws == 1:
         if g_shard.data_ptr() != g_full.data_ptr():
             g_shard.copy_(g_full[:g_shard.numel()])
+    elif _host_staged(g_full, group):
+        out = torch.empty(g_shard.shape, dtype=g_shard.dtype)
+        dist.reduce_scatter_tensor(out, g_full.cpu(), op=dist.ReduceOp.SUM, group=group)
+        g_shard.copy_(out)
     else:
         dist.reduce_scatter_tensor(g_shard, g_full, op=dist.ReduceOp.SUM, group=group)
     if grad_op == "avg" and ws > 1:
@@ -124,7 +135,11 @@ def all_gather_params(w_full: torch.Tensor, w_shard: torch.Tensor, group=None) -
     """Every rank's shard -> w_full on every rank (rank r's shard lands at
     [r * n_shard, (r + 1) * n_shard)).  w_shard may alias its slot in w_full."""
     ws, rank = _world(group)
-    if ws > 1:
+    if ws > 1 and _host_staged(w_full, group):
+        out = torch.empty(w_full.shape, dtype=w_full.dtype)
+        dist.all_gather_into_tensor(out, w_shard.cpu(), group=group)
+        w_full.copy_(out)
+    elif ws > 1:
         dist.all_gather_into_tensor(w_full, w_shard, group=group)
     else:
         n = w_shard.numel()
@@ -138,6 +153,8 @@ def _all_flags(flags: torch.Tensor, group) -> int:
     if ws == 1:
         return int(flags.item())
     bits = torch.stack([(flags >> i) & 1 for i in range(5)]).reshape(-1).to(torch.int32)
+    if _host_staged(bits, group):
+        bits = bits.cpu()
     dist.all_reduce(bits, op=dist.ReduceOp.MAX, group=group)
     v = 0
     for i, b in enumerate(bits.tolist()):

@@ -50,6 +50,14 @@ def ref():
     return Oracle("reference")
 
 
+@pytest.fixture(params=["port", "ref"])
+def checker(request):
+    """The CPU checker of a parity test: the C restatement (oracle/coat_oracle.c)
+    AND the unmodified reference compiled here (oracle/_ref) -- adversarial
+    suites run against both (pin them to the reference itself)."""
+    return request.getfixturevalue(request.param)
+
+
 @pytest.fixture(scope="session")
 def coat():
     from paper_2410_19313_b200 import coatsim

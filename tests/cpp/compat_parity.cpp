@@ -124,6 +124,26 @@ static void test_step() {
     bool threw = false;
     try { coatsim::step(w, g, slot, cfg); } catch (const coatsim::NonFiniteGradient&) { threw = true; }
     CHECK(threw && w.data == w_before && slot.step == 4);
+
+    // OptimizerSlot is a value type (optimizer.hpp:48-52): stepping a copy
+    // twice must leave the original's moments exactly as they were
+    const auto m_before = slot.m(), v_before = slot.v();
+    coatsim::OptimizerSlot copy = slot;
+    auto w2 = w;
+    for (int t = 0; t < 2; ++t) {
+        auto g2 = generate(0, {n}, 0.01, 100.0, 200 + t);
+        for (float& v : g2.data) v *= 1e-3f;
+        coatsim::step(w2, g2, copy, cfg);
+    }
+    CHECK(copy.step == 6 && slot.step == 4);
+    const auto m_after = slot.m(), v_after = slot.v();
+    CHECK(m_after.quantized.codes == m_before.quantized.codes && v_after.quantized.codes == v_before.quantized.codes);
+    CHECK(m_after.quantized.scales == m_before.quantized.scales && v_after.quantized.scales == v_before.quantized.scales);
+    CHECK(copy.m().quantized.codes != m_before.quantized.codes);
+    // copy-assignment deep-copies too
+    coatsim::OptimizerSlot assigned;
+    assigned = slot;
+    CHECK(assigned.mbuf[0] != slot.mbuf[0] && assigned.m().quantized.codes == m_before.quantized.codes);
 }
 
 int main() {

@@ -67,31 +67,31 @@ def _check_state(coat, port, x):
     assert diff.size == 0, (diff[:10], back[diff[:10]], exp[diff[:10]])
 
 
-def test_expand_quantize_m_like(coat, port):
-    _check_state(coat, port, m_like(port, 4096))
+def test_expand_quantize_m_like(coat, port, checker):
+    _check_state(coat, checker, m_like(port, 4096))
 
 
-def test_expand_quantize_v_like(coat, port):
-    _check_state(coat, port, v_like(4096))
+def test_expand_quantize_v_like(coat, port, checker):
+    _check_state(coat, checker, v_like(4096))
 
 
-def test_expand_quantize_special_groups(coat, port):
-    _check_state(coat, port, special_groups())
+def test_expand_quantize_special_groups(coat, port, checker):
+    _check_state(coat, checker, special_groups())
 
 
-def test_expand_quantize_uniform_log(coat, port):
+def test_expand_quantize_uniform_log(coat, port, checker):
     for rr, seed in ((1e2, 5), (1e4, 6), (1e6, 7), (2.0, 8)):
-        _check_state(coat, port, port.generate(2, (128 * 512,), 0.0, rr, seed))
+        _check_state(coat, checker, port.generate(2, (128 * 512,), 0.0, rr, seed))
 
 
-def test_expand_quantize_large_random(coat, port):
+def test_expand_quantize_large_random(coat, port, checker):
     """Many groups with k spread across [1, 20]: exactness at scale."""
     r = rng(1234)
     groups = 1 << 14
     ranges = np.exp(r.uniform(np.log(1.05), np.log(1e7), groups))
     x = np.concatenate([np.exp(r.uniform(-0.5 * np.log(q), 0.5 * np.log(q), 128))
                         * r.choice([-1, 1], 128) * 10 ** r.uniform(-9, 2) for q in ranges])
-    _check_state(coat, port, x.astype(np.float32))
+    _check_state(coat, checker, x.astype(np.float32))
 
 
 def test_expand_quantize_cfg1_size(coat, port):

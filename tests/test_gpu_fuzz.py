@@ -55,12 +55,12 @@ def _mixed(r, n, scale=1.0):
 
 
 @pytest.mark.parametrize("case", range(40))
-def test_fuzz_k1_steps(coat, port, case):
+def test_fuzz_k1_steps(coat, port, checker, case):
     r = np.random.default_rng(1000 + case)
     n = int(r.choice([128 * r.integers(1, 40), 1792 * r.integers(1, 200) + r.integers(0, 1792),
                       int(r.integers(1000, 400_000))]))
     w = _mixed(r, n, 0.02)
-    m, v = port.make_slot(n)
+    m, v = checker.make_slot(n)
     slot = coat.make_slot([n])
     wg = _dev(w)
     cfg = dict(CFG, weight_decay=float(r.choice([0.0, 0.1])), lr=float(r.choice([1e-3, 1e-4])))
@@ -69,7 +69,7 @@ def test_fuzz_k1_steps(coat, port, case):
         g = _mixed(r, n, float(r.choice([1e-3, 1.0, 1e-6])))
         if t == 0:   # the first step always compares fully: keep g*g finite
             g = np.clip(np.nan_to_num(g, posinf=0.0, neginf=0.0), -1e15, 1e15).astype(np.float32)
-        st = port.step(w, g, m, v, t, cfg)
+        st = checker.step(w, g, m, v, t, cfg)
         assert t > 0 or st == 0, (case, st)
         if st != 0:   # the reference throws (e.g. g*g overflow -> NonFiniteInput): so must the GPU
             with pytest.raises(Exception):
@@ -85,7 +85,7 @@ def test_fuzz_k1_steps(coat, port, case):
 
 
 @pytest.mark.parametrize("case", range(40))
-def test_fuzz_mgaq(coat, port, case):
+def test_fuzz_mgaq(coat, port, checker, case):
     import torch
     r = np.random.default_rng(2000 + case)
     G = int(r.choice([0, 16, 32, 64, 128]))
@@ -102,24 +102,24 @@ def test_fuzz_mgaq(coat, port, case):
         return
     geo = coat.QuantGeometry.per_group(G) if G else coat.QuantGeometry.per_tensor()
     q = coat.quantize(xt.cuda(), geo)
-    codes, scales = port.quantize(x, G)
+    codes, scales = checker.quantize(x, G)
     assert np.array_equal(_host(q.codes), codes), case
     assert np.array_equal(_host(q.scales).ravel(), np.asarray(scales).ravel()), case
 
 
 @pytest.mark.parametrize("case", range(20))
-def test_fuzz_dre_round_trip(coat, port, case):
+def test_fuzz_dre_round_trip(coat, port, checker, case):
     r = np.random.default_rng(3000 + case)
     n = 128 * int(r.integers(1, 3000))
     x = _mixed(r, n, float(r.choice([1e-6, 1.0, 1e-30])))
     st = coat.expand_quantize(_dev(x))
-    codes, s, k, c = port.expand_quantize(x)
+    codes, s, k, c = checker.expand_quantize(x)
     assert np.array_equal(_host(st.quantized.codes), codes), case
     assert np.array_equal(_host(st.quantized.scales), s), case
     assert np.array_equal(_host(st.k).view(np.uint32), k.view(np.uint32)), case
     assert np.array_equal(_host(st.c).view(np.uint32), c.view(np.uint32)), case
     back = _host(coat.dequantize_contract(st))
-    assert np.array_equal(back.view(np.uint32), port.dequantize_contract(codes, s, k, c).view(np.uint32)), case
+    assert np.array_equal(back.view(np.uint32), checker.dequantize_contract(codes, s, k, c).view(np.uint32)), case
 
 
 def _moment_state(port, r, n, positive):
@@ -132,7 +132,7 @@ def _moment_state(port, r, n, positive):
 
 
 @pytest.mark.parametrize("case", range(40))
-def test_fuzz_k1_warm_states(coat, port, case):
+def test_fuzz_k1_warm_states(coat, port, checker, case):
     """K1 from random warm states (m, v built by the oracle's expand_quantize of
     mixed distributions: k spread over [1, 20], tiny and huge scales), random
     step counters and AdamW settings."""
@@ -140,8 +140,8 @@ def test_fuzz_k1_warm_states(coat, port, case):
     n = 128 * int(r.integers(1, 2500))
     w = _mixed(r, n, float(r.choice([0.02, 1.0, 1e-6])))
     w = np.clip(np.nan_to_num(w, posinf=0.0, neginf=0.0), -1e30, 1e30).astype(np.float32)
-    m = _moment_state(port, r, n, False)
-    v = _moment_state(port, r, n, True)
+    m = _moment_state(checker, r, n, False)
+    v = _moment_state(checker, r, n, True)
     t0 = int(r.integers(0, 10000))
     cfg = {"beta1": float(r.choice([0.9, 0.8, 0.95])), "beta2": float(r.choice([0.999, 0.99, 0.95])),
            "lr": float(r.choice([1e-3, 3e-4, 1e-2])), "weight_decay": float(r.choice([0.0, 0.1, 0.01])),
@@ -151,7 +151,7 @@ def test_fuzz_k1_warm_states(coat, port, case):
     wg = _dev(w)
     g = _mixed(r, n, float(r.choice([1e-3, 1e-6, 1e-12])))
     g = np.clip(np.nan_to_num(g, posinf=0.0, neginf=0.0), -1e15, 1e15).astype(np.float32)
-    st = port.step(w, g, m, v, t0, cfg)
+    st = checker.step(w, g, m, v, t0, cfg)
     if st != 0:
         with pytest.raises(Exception):
             coat.step(wg, _dev(g), slot, coat.AdamWConfig(**cfg))

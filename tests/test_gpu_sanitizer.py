@@ -1,0 +1,44 @@
+"""GPU: compute-sanitizer over the hot-path kernels ("race
+detection / sanitizers").  racecheck (shared-memory hazards of the mbarrier /
+TMA round pipeline of K1 and the GEMM's staging), synccheck (barrier misuse),
+memcheck (out-of-bounds / misaligned accesses) on small invocations of every
+K1 layout (COAT_K1_EW = 6 / 7 / 8), both forms of coat_quantize_batch and
+both GEMM kernels (CTA pair, single CTA).  Each report is written to
+gpurun_out/sanitizer/ (summaries committed under profiles/r02/)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SANITIZER = "/usr/local/cuda/bin/compute-sanitizer"
+CASES = [("k1", {"COAT_K1_EW": "8"}), ("k1", {"COAT_K1_EW": "7"}), ("k1", {"COAT_K1_EW": "6"}),
+         ("mgaq", {}), ("mgaq", {"COAT_MGAQ_BATCH": "coop"}),
+         ("gemm", {}), ("gemm", {"COAT_GEMM_CTA": "1"})]
+
+
+@pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
+@pytest.mark.parametrize("which,env", CASES, ids=[f"{w}-{'-'.join(f'{k}={v}' for k, v in e.items()) or 'default'}"
+                                                  for w, e in CASES])
+def test_compute_sanitizer_clean(tool, which, env):
+    if not os.path.exists(SANITIZER):
+        pytest.skip("compute-sanitizer not installed")
+    out_dir = os.path.join(ROOT, "gpurun_out", "sanitizer")
+    os.makedirs(out_dir, exist_ok=True)
+    tag = f"{tool}_{which}_" + ("_".join(f"{k}{v}" for k, v in env.items()) or "default")
+    log = os.path.join(out_dir, tag + ".txt")
+    cmd = [SANITIZER, "--tool", tool, "--error-exitcode", "99", "--log-file", log]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report", "all"]
+    cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_workload.py"), which]
+    r = subprocess.run(cmd, cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    report = open(log).read() if os.path.exists(log) else ""
+    assert r.returncode == 0, (r.returncode, report[-3000:], r.stdout[-1000:], r.stderr[-1000:])
+    # --error-exitcode makes any reported error fail the run; the summary line
+    # must say zero (racecheck: "0 hazards displayed (0 errors, ...)")
+    assert "SUMMARY" in report and ("0 errors" in report or "0 hazards" in report), report[-3000:]
+    assert f"sanitize workload {which} ok" in r.stdout

@@ -67,11 +67,11 @@ def run_both(coat, port, n, steps, cfg=CFG, seed=1, warm=None, grad_scale=1e-3):
 
 
 @pytest.mark.parametrize("n", [128, 512, 4096, 5000, 1000 * 128 + 3, 1 << 16])
-def test_step_trajectory_bit_exact(coat, port, n):
-    run_both(coat, port, n, 5)
+def test_step_trajectory_bit_exact(coat, port, checker, n):
+    run_both(coat, checker, n, 5)
 
 
-def test_step_from_warmed_state(coat, port):
+def test_step_from_warmed_state(coat, port, checker):
     """Fixture (B) of SURVEY.md 8(d): m with k ~ 1-3, v with k ~ 5-15, t = 10."""
     groups = 2048
     n = groups * 128
@@ -79,13 +79,13 @@ def test_step_from_warmed_state(coat, port):
     r = rng(22)
     v0 = np.concatenate([np.exp(r.uniform(-0.5 * np.log(q), 0.5 * np.log(q), 128)) * 1e-8
                          for q in r.uniform(2.5, 11.0, groups)]).astype(np.float32)
-    mc, ms, mk, mcc = port.expand_quantize(m0)
-    vc, vs, vk, vcc = port.expand_quantize(v0)
+    mc, ms, mk, mcc = checker.expand_quantize(m0)
+    vc, vs, vk, vcc = checker.expand_quantize(v0)
     warm = ({"codes": mc, "scales": ms, "k": mk, "c": mcc}, {"codes": vc, "scales": vs, "k": vk, "c": vcc})
-    run_both(coat, port, n, 3, warm=warm)
+    run_both(coat, checker, n, 3, warm=warm)
 
 
-def test_step_sparse_zero_and_extreme_groups(coat, port):
+def test_step_sparse_zero_and_extreme_groups(coat, port, checker):
     """Groups the fast paths must hand off exactly: whole zero groups (v' == 0,
     all-zero state), scattered zero gradients (zero-aware extrema), tiny and
     huge gradient groups (IEEE AdamW path, literal contract/pack), through
@@ -93,7 +93,7 @@ def test_step_sparse_zero_and_extreme_groups(coat, port):
     n = 96 * 2048 + 640
     w0 = port.generate(0, (n,), 0.0, 100.0, 5) * np.float32(0.02)
     w_ref = w0.copy()
-    m, v = port.make_slot(n)
+    m, v = checker.make_slot(n)
     slot = coat.make_slot([n])
     w = dev(w0)
     c = coat.AdamWConfig(**CFG)
@@ -106,7 +106,7 @@ def test_step_sparse_zero_and_extreme_groups(coat, port):
         gv[3::41] *= np.float32(1e-30)                            # tiny groups
         gv[5::53] *= np.float32(1e16)                             # huge groups
         gv[7::59, :64] = 0.0
-        assert port.step(w_ref, g, m, v, t, CFG) == 0
+        assert checker.step(w_ref, g, m, v, t, CFG) == 0
         coat.step(w, dev(g), slot, c)
         gm, gvs = gpu_state(slot)
         wd = host(w)
@@ -116,8 +116,8 @@ def test_step_sparse_zero_and_extreme_groups(coat, port):
         assert_state_equal(gvs, v, f"v step {t}")
 
 
-def test_step_without_weight_decay_and_large_grads(coat, port):
-    run_both(coat, port, 1 << 14, 3, cfg=dict(CFG, weight_decay=0.0), grad_scale=1.0)
+def test_step_without_weight_decay_and_large_grads(coat, port, checker):
+    run_both(coat, checker, 1 << 14, 3, cfg=dict(CFG, weight_decay=0.0), grad_scale=1.0)
 
 
 def test_step_kat_first_step(coat):
@@ -148,7 +148,7 @@ def test_nonfinite_grad_leaves_everything_untouched(coat):
     assert slot.step == 1
 
 
-def test_pack_failure_commits_like_reference(coat, port):
+def test_pack_failure_commits_like_reference(coat, port, checker):
     """g*g overflow -> v = inf -> pack_moment(v) throws: params and m committed,
     v and the step counter not (optimizer.cpp:101-114)."""
     import torch
@@ -162,9 +162,9 @@ def test_pack_failure_commits_like_reference(coat, port):
         coat.step(w, g, slot, coat.AdamWConfig(weight_decay=0.1))
     # reference
     wr = np.ones(n, np.float32)
-    m, v = port.make_slot(n)
+    m, v = checker.make_slot(n)
     m0 = {k: a.copy() for k, a in m.items()}
-    assert port.step(wr, host(g), m, v, 0, dict(CFG)) == 3
+    assert checker.step(wr, host(g), m, v, 0, dict(CFG)) == 3
     assert np.array_equal(host(w), wr)
     assert torch.equal(slot.v.quantized.codes, v_before)
     assert np.array_equal(host(slot.m.quantized.codes), m["codes"])
@@ -253,7 +253,7 @@ def test_step_in_place_state_matches_ping_pong(coat, port):
 
 @pytest.mark.parametrize("moment,group,k,code", [("m", 3, 1.0, 0x7F), ("m", 5, 2.5, 0xFF),
                                                   ("v", 7, 3.0, 0x7F), ("v", 9, 1.0, 0xFF)])
-def test_nan_code_in_state_is_a_contract_error(coat, port, moment, group, k, code):
+def test_nan_code_in_state_is_a_contract_error(coat, port, checker, moment, group, k, code):
     """A NaN E4M3 code in the stored state (0x7F / 0xFF) makes unpack (decode,
     fp8.cpp:145-152) throw NonFiniteInput before anything is mutated -- for a
     k == 1 group (exact contract) and a k != 1 group (table contract, where the
@@ -263,9 +263,9 @@ def test_nan_code_in_state_is_a_contract_error(coat, port, moment, group, k, cod
     r = rng(51)
     w0 = (r.standard_normal(n) * 0.02).astype(np.float32)
     g0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
-    m, v = port.make_slot(n)
+    m, v = checker.make_slot(n)
     wr = w0.copy()
-    assert port.step(wr, g0, m, v, 0, CFG) == 0
+    assert checker.step(wr, g0, m, v, 0, CFG) == 0
     st = {"m": m, "v": v}[moment]
     st["codes"][group * 128 + 17] = code
     st["k"][group] = np.float32(k)
@@ -281,11 +281,11 @@ def test_nan_code_in_state_is_a_contract_error(coat, port, moment, group, k, cod
     assert slot.step == 1
     # the reference throws NonFiniteInput as well and leaves w untouched
     w_ref = wr.copy()
-    assert port.step(w_ref, host(g), m, v, 1, CFG) == 3
+    assert checker.step(w_ref, host(g), m, v, 1, CFG) == 3
     assert np.array_equal(w_ref, wr)
 
 
-def test_step_signed_zero_weights_and_grads(coat, port):
+def test_step_signed_zero_weights_and_grads(coat, port, checker):
     """w and g containing +0 and -0 (and groups of them) step exactly like
     the reference: the signs of zero updates follow IEEE as in adamw_update
     (optimizer.cpp:57-68), zero moments pack to +0 (expand.cpp:18-22)."""
@@ -296,7 +296,7 @@ def test_step_signed_zero_weights_and_grads(coat, port):
     w0[::7] = 0.0
     w0[3::7] = -0.0
     w0[128 * 5:128 * 6] = -0.0
-    m, v = port.make_slot(n)
+    m, v = checker.make_slot(n)
     slot = coat.make_slot([n])
     w_ref, w = w0.copy(), dev(w0)
     c = coat.AdamWConfig(**CFG)
@@ -305,7 +305,7 @@ def test_step_signed_zero_weights_and_grads(coat, port):
         g[::5] = -0.0
         g[2::5] = 0.0
         g[128 * 7:128 * 9] = -0.0
-        assert port.step(w_ref, g, m, v, t, CFG) == 0
+        assert checker.step(w_ref, g, m, v, t, CFG) == 0
         coat.step(w, dev(g), slot, c)
         wd = host(w)
         bad = np.nonzero(wd.view(np.uint32) != w_ref.view(np.uint32))[0]
@@ -315,7 +315,7 @@ def test_step_signed_zero_weights_and_grads(coat, port):
         assert_state_equal(gv, v, f"v step {t}")
 
 
-def test_step_subnormal_moment_groups(coat, port):
+def test_step_subnormal_moment_groups(coat, port, checker):
     """Gradients ~1e-21 make v' = (1 - b2) g^2 subnormal; such a group's
     c = sqrt(lo * hi) is subnormal too, and with k > 1 the expanded maximum
     must come from pow(hi / (double)c, k) as in the reference (a float
@@ -328,9 +328,9 @@ def test_step_subnormal_moment_groups(coat, port):
         gg = (r.standard_normal(128) * 10.0 ** r.uniform(-22.5, -21)).astype(np.float32)
         gg[r.random(128) < 0.3] = 0.0
         g[q * 128:(q + 1) * 128] = gg
-    m, v = port.make_slot(n)
+    m, v = checker.make_slot(n)
     w_ref = w0.copy()
-    assert port.step(w_ref, g, m, v, 0, CFG) == 0
+    assert checker.step(w_ref, g, m, v, 0, CFG) == 0
     assert (v["k"] > 1).any() and (v["c"] < 2.0 ** -126).any()   # the case is exercised
     slot = coat.make_slot([n])
     w = dev(w0)
