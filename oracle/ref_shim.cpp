@@ -157,12 +157,14 @@ int step_one(float* w, const float* g, int64_t n, int64_t G, uint8_t* mc, float*
         } catch (...) {
             err = std::current_exception();
         }
-        // The reference mutates params before packing the moments, so a
-        // NonFiniteInput from pack_moment leaves params updated: mirror that.
+        // The reference mutates params before packing the moments and assigns
+        // slot.m before packing v (optimizer.cpp:108-112), so a NonFiniteInput
+        // from pack_moment(v) leaves params AND slot.m updated: write back
+        // whatever the reference object now holds, then report the error.
         std::copy(params.data.begin(), params.data.end(), w);
-        if (err) std::rethrow_exception(err);
         unstate(std::get<ExpandedQuantState>(slot.m), mc, ms, mk, mcc);
         unstate(std::get<ExpandedQuantState>(slot.v), vc, vs, vk, vcc);
+        if (err) std::rethrow_exception(err);
     });
 }
 
