@@ -1093,6 +1093,7 @@ def run_linear(args, extra_mode=False):
         fp8_peak, kind = 2 * bf16_peak, f"2x bf16 (FP8 probe failed: {ex!r:.80})"
     cpu = None if args.no_cpu_baseline else linear_cpu_baseline()
     tf = {k: flop / (per[k] * 1e-3) / 1e12 for k in ("fwd", "dgrad", "wgrad")}
+    upgate = mlp_upgate_compare(L, xc, sx, wc, sw, M, K, N, dev, st)
     out = {
         "metric": "Per-tensor FP8 linear fwd+bwd (cfg4), TFLOP/s", "value": 3 * flop / (ms * 1e-3) / 1e12,
         "unit": "TFLOP/s", "n_gpus": 1, "steps": reps, "warmup": args.warmup, "ms_per_step": ms,
@@ -1107,8 +1108,68 @@ def run_linear(args, extra_mode=False):
                      "bwd_frac_of_bf16": {"dgrad": tf["dgrad"] / bf16_peak, "wgrad": tf["wgrad"] / bf16_peak},
                      "bf16_peak": bf16_peak, "bf16_peak_kind": bf16_kind},
         "cpu_baseline": cpu, "clocks": sampler.summary(), "gpu_launches": 9 * reps,
+        "mlp_upgate": upgate,
     }
     return out
+
+
+def mlp_upgate_compare(L, xc, sx, wc, sw, M, K, N, dev, st):
+    """the MLP's gate and up projections (flow.cpp:599-600,
+    both x . W with W (5120, 13824) -- the cfg4 weight serves as both) followed
+    by the SiLU*mul block's quantizers (flow.cpp:603-612).  Unfused: two
+    forward GEMMs writing fp32 gate / up, then coat_silu_mul_quant reading them.
+    Fused: coat_fp8_upgate_silu_quant (one GEMM, quantizers in the epilogue,
+    then the per-tensor down.in pass from the codes).  Same outputs (tested)."""
+    import torch
+    u8 = lambda: torch.empty(M, N, dtype=torch.uint8, device=dev)
+    sc = lambda: torch.empty(M * N // 16, dtype=torch.int16, device=dev)
+    gc, gs, scd, ss, uc, us, pc = u8(), sc(), u8(), sc(), u8(), sc(), u8()
+    ps = torch.empty(1, dtype=torch.int16, device=dev)
+    amax = torch.empty(1, dtype=torch.int32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    gate = torch.empty(M, N, dtype=torch.float32, device=dev)
+    up = torch.empty(M, N, dtype=torch.float32, device=dev)
+
+    def unfused():
+        s = st.cuda_stream
+        for y in (gate, up):
+            assert L.coat_fp8_linear_fwd(xc.data_ptr(), sx.data_ptr(), wc.data_ptr(), sw.data_ptr(), M, K, N,
+                                         y.data_ptr(), s) == 0
+        assert L.coat_silu_mul_quant(gate.data_ptr(), up.data_ptr(), 0, M, N, gc.data_ptr(), gs.data_ptr(),
+                                     scd.data_ptr(), ss.data_ptr(), uc.data_ptr(), us.data_ptr(), pc.data_ptr(),
+                                     ps.data_ptr(), None, amax.data_ptr(), flags.data_ptr(), s) == 0
+
+    def fused():
+        assert L.coat_fp8_upgate_silu_quant(xc.data_ptr(), sx.data_ptr(), wc.data_ptr(), sw.data_ptr(),
+                                            wc.data_ptr(), sw.data_ptr(), M, K, N, gc.data_ptr(), gs.data_ptr(),
+                                            scd.data_ptr(), ss.data_ptr(), uc.data_ptr(), us.data_ptr(),
+                                            pc.data_ptr(), ps.data_ptr(), None, None, None, amax.data_ptr(),
+                                            flags.data_ptr(), st.cuda_stream) == 0, L.coat_last_error()
+
+    res = {}
+    for name, fn in (("unfused", unfused), ("fused", fused), ("unfused_b", unfused), ("fused_b", fused)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        reps = _reps_for(fn, 0.5, 5)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(0)
+        with sampler:
+            e0.record(st)
+            for _ in range(reps):
+                fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        key = name.rstrip("_b")
+        res[key] = min(res.get(key, 1e9), ms)
+        res[key + "_clocks"] = sampler.summary()
+    flop = 2 * 2.0 * M * N * K
+    return {"what": "gate+up GEMMs (x[8192,5120] . W[5120,13824] twice) + SiLU*mul quantizers -> silu.in, "
+                    "mul.in.silu, mul.in.up (1x16) + down.in (per-tensor)",
+            "unfused_ms": res["unfused"], "fused_ms": res["fused"],
+            "fused_tflops": flop / (res["fused"] * 1e-3) / 1e12, "speedup": res["unfused"] / res["fused"],
+            "clocks_fused": res["fused_clocks"], "clocks_unfused": res["unfused_clocks"]}
 
 
 if __name__ == "__main__":

@@ -254,6 +254,28 @@ coat_status coat_nccl_comm_destroy(void* nccl_comm);
 coat_status coat_fp8_linear_fwd(const uint8_t* x_codes, const uint16_t* d_sx, const uint8_t* w_codes,
                                 const uint16_t* d_sw, int64_t M, int64_t K, int64_t N, float* y,
                                 void* stream);
+/* The same y quantized per group of 16 in the GEMM epilogue:
+ * y_codes [M,N] / y_scales [M,N/16] = quantize(y, per_group(16)) bit for bit
+ * as coat_quantize_per_group would encode coat_fp8_linear_fwd's y; y never
+ * reaches HBM unless y_out (fp32, may be NULL) is given.  Non-finite y ->
+ * NONFINITE_INPUT in *d_flags (quantize.cpp:91). */
+coat_status coat_fp8_linear_fwd_q16(const uint8_t* x_codes, const uint16_t* d_sx, const uint8_t* w_codes,
+                                    const uint16_t* d_sw, int64_t M, int64_t K, int64_t N, uint8_t* y_codes,
+                                    uint16_t* y_scales, float* y_out, uint32_t* d_flags, void* stream);
+/* The MLP's gate/up projections and the SiLU*mul block in one tcgen05 GEMM
+ * (flow.cpp:599-610): gate = DQ(x) . DQ(W_gate), up = DQ(x) . DQ(W_up) (W (H, I)
+ * row-major), the epilogue writes silu.in = Q_g16(gate), mul.in.silu =
+ * Q_g16(silu(DQ(silu.in))), mul.in.up = Q_g16(up) and the product absmax; a
+ * second pass encodes down.in = Q_t(DQ(mul.in.silu) * DQ(mul.in.up)) from the
+ * codes.  Outputs equal coat_silu_mul_quant applied to the two
+ * coat_fp8_linear_fwd outputs.  gate_out / up_out / p_out: optional fp32
+ * side outputs (NULL: gate and up never reach HBM).  I % 16 == 0. */
+coat_status coat_fp8_upgate_silu_quant(const uint8_t* x_codes, const uint16_t* d_sx, const uint8_t* wg_codes,
+                                       const uint16_t* d_swg, const uint8_t* wu_codes, const uint16_t* d_swu,
+                                       int64_t M, int64_t H, int64_t I, uint8_t* g_codes, uint16_t* g_scales,
+                                       uint8_t* s_codes, uint16_t* s_scales, uint8_t* u_codes, uint16_t* u_scales,
+                                       uint8_t* p_codes, uint16_t* d_p_scale, float* gate_out, float* up_out,
+                                       float* p_out, uint32_t* d_amax_bits, uint32_t* d_flags, void* stream);
 /* dX[M,K] (bf16) = bf16(dY[M,N] . W_used^T), W_used = s_w * w_dec (flow.cpp:636);
  * w_dec = coat_decode_e4m3_bf16(w_codes), exact. */
 coat_status coat_linear_bwd_dgrad(const uint16_t* dy_bf16, const uint16_t* w_dec_bf16,

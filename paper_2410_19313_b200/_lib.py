@@ -98,6 +98,8 @@ _SIGS = {
                                   _i64, _vp], _int),
     "coat_set_fallback_counter": ([_vp], _int),
     "coat_fp8_linear_fwd": ([_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp], _int),
+    "coat_fp8_linear_fwd_q16": ([_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _int),
+    "coat_fp8_upgate_silu_quant": ([_vp] * 6 + [_i64, _i64, _i64] + [_vp] * 14, _int),
     "coat_linear_bwd_dgrad": ([_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp], _int),
     "coat_linear_bwd_wgrad": ([_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp], _int),
     "coat_decode_e4m3_bf16": ([_vp, _vp, _i64, _vp], _int),

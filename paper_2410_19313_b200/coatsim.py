@@ -739,6 +739,67 @@ def fp8_linear(qx: QuantizedTensor, qw: QuantizedTensor) -> torch.Tensor:
     return y
 
 
+def fp8_linear_q16(qx: QuantizedTensor, qw: QuantizedTensor, return_y: bool = False):
+    """quantize(fp8_linear(qx, qw), per_group(16)) with the quantizer in the
+    GEMM epilogue: the product never reaches HBM unless
+    return_y (then also the fp32 y)."""
+    _per_tensor(qx, "fp8_linear_q16")
+    _per_tensor(qw, "fp8_linear_q16")
+    (M, K), (K2, N) = qx.source_shape, qw.source_shape
+    if K != K2:
+        raise ShapeMismatch("fp8_linear_q16: inner dimensions differ")
+    if N % 16:
+        raise GeometryMismatch("per-group: last dim not divisible by group size")
+    dev = qx.codes.device
+    yc = torch.empty(M, N, dtype=torch.uint8, device=dev)
+    ys = torch.empty(M * N // 16, dtype=torch.bfloat16, device=dev)
+    y = torch.empty(M, N, dtype=torch.float32, device=dev) if return_y else None
+    fl = _Flags(dev)
+    _check(L.coat_fp8_linear_fwd_q16(qx.codes.data_ptr(), qx.scales.data_ptr(), qw.codes.data_ptr(),
+                                     qw.scales.data_ptr(), M, K, N, yc.data_ptr(), ys.data_ptr(), _ptr(y), fl.ptr,
+                                     _stream()))
+    fl.raise_if_set("fp8_linear_q16")
+    q = QuantizedTensor(yc, ys, QuantGeometry.per_group(16), Fp8Tag.E4M3, (M, N))
+    return (q, y) if return_y else q
+
+
+def fp8_upgate_silu(qx: QuantizedTensor, qw_gate: QuantizedTensor, qw_up: QuantizedTensor,
+                    return_fp32: bool = False):
+    """The MLP's gate/up projections and the SiLU*mul block (flow.cpp:599-612)
+    as ONE tcgen05 GEMM whose epilogue quantizes: returns the silu.in,
+    mul.in.silu, mul.in.up (per-group 1x16) and down.in (per-tensor) records
+    -- equal to silu_mul_quantize(fp8_linear(qx, qw_gate), fp8_linear(qx,
+    qw_up)) -- [, gate, up, prod] (fp32) with return_fp32."""
+    for q, what in ((qx, "x"), (qw_gate, "W_gate"), (qw_up, "W_up")):
+        _per_tensor(q, f"fp8_upgate_silu {what}")
+    (M, H), (H2, I) = qx.source_shape, qw_gate.source_shape
+    if H != H2 or tuple(qw_up.source_shape) != (H, I):
+        raise ShapeMismatch("fp8_upgate_silu: x (M, H), W_gate and W_up (H, I)")
+    if I % 16:
+        raise GeometryMismatch("per-group: last dim not divisible by group size")
+    dev = qx.codes.device
+    mk = lambda: (torch.empty(M, I, dtype=torch.uint8, device=dev),
+                  torch.empty(M * I // 16, dtype=torch.bfloat16, device=dev))
+    (gc, gs), (sc, ss), (uc, us) = mk(), mk(), mk()
+    pc = torch.empty(M, I, dtype=torch.uint8, device=dev)
+    ps = torch.empty(1, dtype=torch.bfloat16, device=dev)
+    amax = torch.empty(1, dtype=torch.int32, device=dev)
+    f32 = (lambda: torch.empty(M, I, dtype=torch.float32, device=dev)) if return_fp32 else (lambda: None)
+    g, u, p = f32(), f32(), f32()
+    fl = _Flags(dev)
+    _check(L.coat_fp8_upgate_silu_quant(qx.codes.data_ptr(), qx.scales.data_ptr(), qw_gate.codes.data_ptr(),
+                                        qw_gate.scales.data_ptr(), qw_up.codes.data_ptr(), qw_up.scales.data_ptr(),
+                                        M, H, I, gc.data_ptr(), gs.data_ptr(), sc.data_ptr(), ss.data_ptr(),
+                                        uc.data_ptr(), us.data_ptr(), pc.data_ptr(), ps.data_ptr(), _ptr(g), _ptr(u),
+                                        _ptr(p), amax.data_ptr(), fl.ptr, _stream()))
+    fl.raise_if_set("fp8_upgate_silu")
+    g16, shp = QuantGeometry.per_group(16), (M, I)
+    out = (QuantizedTensor(gc, gs, g16, Fp8Tag.E4M3, shp), QuantizedTensor(sc, ss, g16, Fp8Tag.E4M3, shp),
+           QuantizedTensor(uc, us, g16, Fp8Tag.E4M3, shp),
+           QuantizedTensor(pc, ps, QuantGeometry.per_tensor(), Fp8Tag.E4M3, shp))
+    return out + (g, u, p) if return_fp32 else out
+
+
 def linear_dgrad(dy: torch.Tensor, qw: QuantizedTensor, w_dec: torch.Tensor | None = None) -> torch.Tensor:
     """dX = bf16(dY . W_used^T) (flow.cpp:636); dY is BF16 and not quantized."""
     _per_tensor(qw, "linear_dgrad")

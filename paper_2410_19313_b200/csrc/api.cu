@@ -414,6 +414,36 @@ coat_status coat_fp8_linear_fwd(const uint8_t* x_codes, const uint16_t* d_sx, co
     return cuda_status(launch_fp8_linear_fwd(x_codes, d_sx, w_codes, d_sw, int(M), int(K), int(N), y, S(stream)));
 }
 
+coat_status coat_fp8_linear_fwd_q16(const uint8_t* x_codes, const uint16_t* d_sx, const uint8_t* w_codes,
+                                    const uint16_t* d_sw, int64_t M, int64_t K, int64_t N, uint8_t* y_codes,
+                                    uint16_t* y_scales, float* y_out, uint32_t* d_flags, void* stream) {
+    const coat_status st = check_linear(M, K, N, x_codes, w_codes, y_codes);
+    if (st != COAT_OK) return st;
+    if (!y_scales) return fail(COAT_ERR_INVALID, "linear_fwd_q16: NULL scales");
+    if (y_out && !a16(y_out)) return fail(COAT_ERR_INVALID, "linear_fwd_q16: y_out must be 16-byte aligned");
+    return cuda_status(launch_fp8_linear_fwd_q16(x_codes, d_sx, w_codes, d_sw, int(M), int(K), int(N), y_codes,
+                                                 y_scales, y_out, d_flags, S(stream)));
+}
+
+coat_status coat_fp8_upgate_silu_quant(const uint8_t* x_codes, const uint16_t* d_sx, const uint8_t* wg_codes,
+                                       const uint16_t* d_swg, const uint8_t* wu_codes, const uint16_t* d_swu,
+                                       int64_t M, int64_t H, int64_t I, uint8_t* g_codes, uint16_t* g_scales,
+                                       uint8_t* s_codes, uint16_t* s_scales, uint8_t* u_codes, uint16_t* u_scales,
+                                       uint8_t* p_codes, uint16_t* d_p_scale, float* gate_out, float* up_out,
+                                       float* p_out, uint32_t* d_amax_bits, uint32_t* d_flags, void* stream) {
+    coat_status st = check_linear(M, H, I, x_codes, wg_codes, g_codes);
+    if (st != COAT_OK) return st;
+    if (!wu_codes || !g_scales || !s_codes || !s_scales || !u_codes || !u_scales || !p_codes || !d_p_scale ||
+        !d_amax_bits)
+        return fail(COAT_ERR_INVALID, "upgate_silu_quant: NULL buffer");
+    if (!a16(wu_codes) || !a16(s_codes) || !a16(u_codes) || !a16(p_codes) || (gate_out && !a16(gate_out)) ||
+        (up_out && !a16(up_out)) || (p_out && !a16(p_out)) || (!gate_out != !up_out))
+        return fail(COAT_ERR_INVALID, "upgate_silu_quant: 16-byte aligned buffers; gate_out and up_out together");
+    UpGateArgs a{x_codes, d_sx, wg_codes, d_swg, wu_codes, d_swu, M, H, I, g_codes, g_scales, s_codes, s_scales,
+                 u_codes, u_scales, p_codes, d_p_scale, gate_out, up_out, p_out, d_amax_bits, d_flags};
+    return cuda_status(launch_fp8_upgate_silu(a, S(stream)));
+}
+
 coat_status coat_linear_bwd_dgrad(const uint16_t* dy_bf16, const uint16_t* w_dec_bf16, const uint16_t* d_sw,
                                   int64_t M, int64_t K, int64_t N, uint16_t* dx_bf16, void* stream) {
     const coat_status st = check_linear(M, K, N, dy_bf16, w_dec_bf16, dx_bf16);

@@ -73,6 +73,26 @@ coat_status load_slot_impl(const char* path, const int64_t* shape, int rank, int
 // tcgen05 GEMMs (gemm_tcgen05.cu)
 cudaError_t launch_fp8_linear_fwd(const uint8_t* xc, const uint16_t* sx, const uint8_t* wc, const uint16_t* sw, int M,
                                   int K, int N, float* y, cudaStream_t st);
+cudaError_t launch_fp8_linear_fwd_q16(const uint8_t* xc, const uint16_t* sx, const uint8_t* wc, const uint16_t* sw,
+                                      int M, int K, int N, uint8_t* y_codes, uint16_t* y_scales, float* y_out,
+                                      uint32_t* flags, cudaStream_t st);
+struct UpGateArgs {
+    const uint8_t* xc;      // upgate.in codes [M, H], per-tensor scale *sx
+    const uint16_t* sx;
+    const uint8_t* wg;      // W_gate codes (H, I) row-major, scale *s_wg
+    const uint16_t* s_wg;
+    const uint8_t* wu;      // W_up codes (H, I), scale *s_wu
+    const uint16_t* s_wu;
+    int64_t M, H, I;
+    uint8_t* gcodes; uint16_t* gscales;   // silu.in
+    uint8_t* scodes; uint16_t* sscales;   // mul.in.silu
+    uint8_t* ucodes; uint16_t* uscales;   // mul.in.up
+    uint8_t* pcodes; uint16_t* pscale;    // down.in (per-tensor)
+    float* gate_out; float* up_out; float* pout;   // optional fp32 side outputs (tests)
+    uint32_t* amax_bits;
+    uint32_t* flags;
+};
+cudaError_t launch_fp8_upgate_silu(const UpGateArgs& a, cudaStream_t st);
 cudaError_t launch_linear_dgrad(const uint16_t* dy, const uint16_t* wd, const uint16_t* sw, int M, int K, int N,
                                 uint16_t* dx, cudaStream_t st);
 cudaError_t launch_linear_wgrad(const uint16_t* xd, const uint16_t* sx, const uint16_t* dy, int M, int K, int N,
@@ -129,6 +149,11 @@ struct SiluBlockArgs {
 };
 cudaError_t launch_rmsnorm_block(const RmsBlockArgs& a, cudaStream_t stream);
 cudaError_t launch_silu_mul_block(const SiluBlockArgs& a, cudaStream_t stream);
+// pass 2 of the SiLU*mul block alone: down.in = Q_t(DQ(s) * DQ(u)) from the
+// global product absmax (*amax_bits)
+cudaError_t launch_silu_mul_pass2(const uint8_t* scodes, const uint16_t* sscales, const uint8_t* ucodes,
+                                  const uint16_t* uscales, int64_t n, const uint32_t* amax_bits, uint8_t* pcodes,
+                                  uint16_t* pscale, float* pout, uint32_t* flags, cudaStream_t stream);
 
 // backward-side MGAQ pieces (mgaq_bwd.cu)
 cudaError_t launch_transpose_dequant(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,

@@ -34,6 +34,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "act_quant.cuh"
 #include "coat_device.cuh"
 #include "coat_internal.h"
 
@@ -61,6 +62,34 @@ struct Geo {
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Epilogue kinds.
+enum : int {
+    kOutF32 = 0,      // out fp32 [M, N]
+    kOutBf16 = 1,     // out bf16 [M, N]
+    kOutQ16 = 2,      // per-group (1x16) E4M3 codes + BF16 scales of y (quantize(y, per_group(16)))
+    kOutUpGate = 3,   // the fused gate/up projection + SiLU*mul quantizers (see EpiQ)
+};
+
+// Quantizing epilogues (kOutQ16 / kOutUpGate).  Row strides: ldc codes per row
+// (= N), ldc / 16 scales per row.
+//   kOutQ16:    c0/s0 = Q_g16(y);  y0 (may be NULL) = y (fp32)
+//   kOutUpGate: B = [W_gate | W_up] per 128-column block (tile n covers gate and
+//               up columns [128n, 128n+128)); with g = y_gate, u = y_up:
+//               c0/s0 = Q_g16(g) (silu.in), c1/s1 = Q_g16(silu(DQ(c0))) (mul.in.silu),
+//               c2/s2 = Q_g16(u) (mul.in.up), *amax_bits = max |DQ(c1) * DQ(c2)|
+//               (NaN ignored) for the per-tensor down.in pass; y0 / y1 (may be
+//               NULL) = g / u (fp32)
+struct EpiQ {
+    uint8_t* c0; uint16_t* s0;
+    uint8_t* c1; uint16_t* s1;
+    uint8_t* c2; uint16_t* s2;
+    float* y0; float* y1;
+    const uint16_t* scale_b1;   // BF16 device scale of W_up (kOutUpGate)
+    uint32_t* amax_bits;
+    uint32_t* flags;            // kFlagNonFiniteInput (quantize.cpp:91)
+    int64_t ldc;
+};
+
 struct Params {
     int M, N, K;               // K in elements
     int tiles_m, tiles_n, k_blocks;
@@ -69,6 +98,7 @@ struct Params {
     const uint16_t* scale_b;
     void* out;
     int64_t ldo;               // elements
+    EpiQ q;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -184,9 +214,29 @@ __host__ __device__ constexpr uint32_t instr_desc(bool f8, bool a_mn, bool b_mn,
            ((b_mn ? 1u : 0u) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
-template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16, int kCta>
+// Per-group (1x16) quantization of one 16-column group of y held by this
+// thread (quantize.cpp:89-111 with G = 16: NaN/Inf -> non-finite flag).
+__device__ __forceinline__ uint32_t quant16_store(const aq::Chunk16& y, uint8_t* codes, uint16_t* scale, float nz,
+                                                  bool store) {
+    float m = aq::fmax3_nan_(fabsf(y.v[0]), fabsf(y.v[1]), fabsf(y.v[2]));
+#pragma unroll
+    for (int i = 3; i < 15; i += 2) m = aq::fmax3_nan_(m, fabsf(y.v[i]), fabsf(y.v[i + 1]));
+    m = aq::fmax3_nan_(m, fabsf(y.v[15]), 0.0f);
+    float s, rs;
+    aq::group_scale_fast(f2u(m), s, rs);
+    const uint4 cw = aq::encode16(y, s, rs, nz);
+    if (store) {
+        *reinterpret_cast<uint4*>(codes) = cw;
+        *scale = float_to_bf16_bits_exact(s);
+    }
+    return f2u(m) >= 0x7F800000u ? 1u : 0u;
+}
+
+template <bool kF8, bool kAMN, bool kBMN, int kOut, int kCta>
 __global__ void __launch_bounds__(THREADS, 1)
-gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params P) {
+gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+            const __grid_constant__ CUtensorMap map_b2, Params P) {
+    static_assert(kOut != kOutUpGate || (kF8 && kBMN), "gate/up epilogue: FP8 forward, W (K, N) row-major");
     using G = Geo<kCta>;
     constexpr int STAGES = G::STAGES;
     constexpr int STAGE_BYTES = G::STAGE_BYTES;
@@ -263,7 +313,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                             for (int c = 0; c < BM * ESZ / 128; ++c)
                                 tma_load_2d(sa + c * BK * 128, &map_a, m0 + c * (128 / ESZ), k0, &full[stage]);
                         }
-                        if (!kBMN) {
+                        if (kOut == kOutUpGate) {
+                            // gate columns then up columns of the same 128-column block
+                            tma_load_2d(sb, &map_b, nb * 128, k0, &full[stage]);
+                            tma_load_2d(sb + BK * 128, &map_b2, nb * 128, k0, &full[stage]);
+                        } else if (!kBMN) {
                             tma_load_2d(sb, &map_b, k0, n0, &full[stage]);
                         } else {
 #pragma unroll
@@ -281,7 +335,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                             for (int c = 0; c < BM * ESZ / 128; ++c)
                                 tma_load_2d_pair(sa + c * BK * 128, &map_a, m0 + c * (128 / ESZ), k0, fb);
                         }
-                        if (!kBMN) {
+                        if (kOut == kOutUpGate) {
+                            // the leader stages the gate columns, its partner the up columns
+                            tma_load_2d_pair(sb, rank == 0 ? &map_b : &map_b2, nb * 128, k0, fb);
+                        } else if (!kBMN) {
                             tma_load_2d_pair(sb, &map_b, k0, n0, fb);
                         } else {
 #pragma unroll
@@ -348,7 +405,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const uint32_t tempty_leader0 = kCta == 2 ? cluster_addr(&tempty[0], 0) : 0u;
         float alpha = P.alpha;
         if (P.scale_a) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_a));
+        float alpha_u = alpha;
         if (P.scale_b) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_b));
+        if (kOut == kOutUpGate && P.q.scale_b1) alpha_u = __fmul_rn(alpha_u, bf16_bits_to_float(*P.q.scale_b1));
+        uint32_t bad = 0;
+        float amp = 0.0f;   // kOutUpGate: max |product| (max.f32: NaN ignored, Inf kept)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = tile0; tile < ntiles; tile += tstep) {
@@ -357,14 +418,82 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             tc_fence_after();
             const int row = mb * G::TILE_M + row_in_tile;
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * ACC_COLS);
+            if (kOut == kOutUpGate) {
+                // accumulator columns [0, 128): gate, [128, 256): up, of output columns nb*128 + j
+                const bool live = row < P.M;
+                const int64_t rq = live ? row : 0;
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t rg[32], ru[32];
+                    tmem_ld32(taddr + uint32_t(c * 32), rg);
+                    tmem_ld32(taddr + uint32_t(128 + c * 32), ru);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = nb * 128 + c * 32 + h * 16;
+                        if (col >= P.N) break;   // warp-uniform (N % 16 == 0)
+                        aq::Chunk16 gv, uv;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            gv.v[i] = __fmul_rn(alpha, u2f(rg[16 * h + i]));
+                            uv.v[i] = __fmul_rn(alpha_u, u2f(ru[16 * h + i]));
+                        }
+                        if (live && P.q.y0) {
+                            float4* o = reinterpret_cast<float4*>(P.q.y0 + rq * P.q.ldc + col);
+                            float4* o1 = reinterpret_cast<float4*>(P.q.y1 + rq * P.q.ldc + col);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                o[k] = make_float4(gv.v[4 * k], gv.v[4 * k + 1], gv.v[4 * k + 2], gv.v[4 * k + 3]);
+                                o1[k] = make_float4(uv.v[4 * k], uv.v[4 * k + 1], uv.v[4 * k + 2], uv.v[4 * k + 3]);
+                            }
+                        }
+                        const int64_t co = rq * P.q.ldc + col, so = rq * (P.q.ldc >> 4) + (col >> 4);
+                        uint4 cw;
+                        uint16_t sbits;
+                        bad |= aq::quant_dq16(gv, cw, sbits, -0.0f);   // silu.in
+                        if (live) { *reinterpret_cast<uint4*>(P.q.c0 + co) = cw; P.q.s0[so] = sbits; }
+                        aq::silu16(gv, -0.0f);
+                        bad |= aq::quant_dq16(gv, cw, sbits, -0.0f);   // mul.in.silu
+                        if (live) { *reinterpret_cast<uint4*>(P.q.c1 + co) = cw; P.q.s1[so] = sbits; }
+                        bad |= aq::quant_dq16(uv, cw, sbits, -0.0f);   // mul.in.up
+                        if (live) { *reinterpret_cast<uint4*>(P.q.c2 + co) = cw; P.q.s2[so] = sbits; }
+                        if (live) {
+#pragma unroll
+                            for (int i = 0; i < 16; i += 2) {
+                                const F2 pr = f2_mul(F2{gv.v[i], gv.v[i + 1]}, F2{uv.v[i], uv.v[i + 1]}, -0.0f);
+                                asm("max.f32 %0, %1, %2, %3;" : "=f"(amp) : "f"(amp), "f"(fabsf(pr.x)), "f"(fabsf(pr.y)));
+                            }
+                        }
+                    }
+                }
+            } else
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
                 tmem_ld32(taddr + uint32_t(c * 32), r);
                 tmem_wait_ld();
                 const int col0 = nb * BN + c * 32;
-                if (row < P.M) {
-                    if (!kOutBf16) {
+                if (kOut == kOutQ16) {
+                    const bool live = row < P.M;
+                    const int64_t rq = live ? row : 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = col0 + h * 16;
+                        if (col >= P.N) break;   // warp-uniform (N % 16 == 0)
+                        aq::Chunk16 y;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) y.v[i] = __fmul_rn(alpha, u2f(r[16 * h + i]));
+                        if (live && P.q.y0) {
+                            float4* o = reinterpret_cast<float4*>(P.q.y0 + rq * P.q.ldc + col);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                o[k] = make_float4(y.v[4 * k], y.v[4 * k + 1], y.v[4 * k + 2], y.v[4 * k + 3]);
+                        }
+                        bad |= quant16_store(y, P.q.c0 + rq * P.q.ldc + col, P.q.s0 + rq * (P.q.ldc >> 4) + (col >> 4),
+                                             -0.0f, live) & (live ? 1u : 0u);
+                    }
+                } else if (row < P.M) {
+                    if (kOut == kOutF32) {
                         float* o = static_cast<float*>(P.out) + int64_t(row) * P.ldo + col0;
                         if (col0 + 32 <= P.N) {
 #pragma unroll
@@ -408,6 +537,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 acc_phase ^= 1u;
             }
         }
+        if (kOut == kOutUpGate) {
+            const uint32_t m = warp_max_u32(f2u(amp));
+            if (lane == 0 && m) atomicMax(P.q.amax_bits, m);
+        }
+        if (kOut >= kOutQ16 && P.q.flags && __reduce_or_sync(0xFFFFFFFFu, bad) && lane == 0)
+            atomicOr(P.q.flags, kFlagNonFiniteInput);
     }
     tc_fence_before();
     if (kCta == 2) cluster_sync_all();   // no CTA of the pair leaves while the other may still signal it
@@ -451,19 +586,23 @@ bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t c
     return r == CUDA_SUCCESS;
 }
 
-template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16, int kCta>
-cudaError_t run_cta(const void* a, const void* b, int M, int N, int K, float alpha, const uint16_t* sa,
-                    const uint16_t* sb, void* out, int64_t ldo, cudaStream_t stream) {
+template <bool kF8, bool kAMN, bool kBMN, int kOut, int kCta>
+cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, int K, float alpha,
+                    const uint16_t* sa, const uint16_t* sb, void* out, int64_t ldo, const EpiQ& q,
+                    cudaStream_t stream) {
     using G = Geo<kCta>;
     constexpr int ESZ = kF8 ? 1 : 2;
     constexpr int BK = BKB / ESZ;
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mb2;
     // A logical [M x K]: K-major memory [M][K]; MN-major memory [K][M]
     const bool ok_a = !kAMN ? make_map(&ma, a, ESZ, M, K, BK, BM) : make_map(&ma, a, ESZ, K, M, 128 / ESZ, BK);
     const bool ok_b =
         !kBMN ? make_map(&mb, b, ESZ, N, K, BK, G::BN_L) : make_map(&mb, b, ESZ, K, N, 128 / ESZ, BK);
-    if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-    auto kern = gemm_kernel<kF8, kAMN, kBMN, kOutBf16, kCta>;
+    // kOutUpGate: the up weight (same geometry as the gate weight); else a copy of B (unused)
+    const bool ok_b2 = kOut == kOutUpGate ? make_map(&mb2, b2, ESZ, K, N, 128 / ESZ, BK) : true;
+    if (!ok_a || !ok_b || !ok_b2) return cudaErrorInvalidValue;
+    if (kOut != kOutUpGate) mb2 = mb;
+    auto kern = gemm_kernel<kF8, kAMN, kBMN, kOut, kCta>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -477,18 +616,19 @@ cudaError_t run_cta(const void* a, const void* b, int M, int N, int K, float alp
     P.N = N;
     P.K = K;
     P.tiles_m = (M + G::TILE_M - 1) / G::TILE_M;
-    P.tiles_n = (N + BN - 1) / BN;
+    P.tiles_n = kOut == kOutUpGate ? (N + 127) / 128 : (N + BN - 1) / BN;
     P.k_blocks = (K + BK - 1) / BK;
     P.alpha = alpha;
     P.scale_a = sa;
     P.scale_b = sb;
     P.out = out;
     P.ldo = ldo;
+    P.q = q;
     const int ntiles = P.tiles_m * P.tiles_n;
     const int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
     const int grid = kCta * (ntiles < units ? ntiles : units);
     if (kCta == 1) {
-        kern<<<grid, THREADS, G::SMEM_BYTES, stream>>>(ma, mb, P);
+        kern<<<grid, THREADS, G::SMEM_BYTES, stream>>>(ma, mb, mb2, P);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -503,7 +643,7 @@ cudaError_t run_cta(const void* a, const void* b, int M, int N, int K, float alp
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, ma, mb, P);
+    return cudaLaunchKernelEx(&cfg, kern, ma, mb, mb2, P);
 }
 
 // COAT_GEMM_CTA=1 forces the single-CTA kernel (A/B comparisons).
@@ -515,12 +655,13 @@ inline int pair_mode() {
     return v;
 }
 
-template <bool kF8, bool kAMN, bool kBMN, bool kOutBf16>
+template <bool kF8, bool kAMN, bool kBMN, int kOut>
 cudaError_t run(const void* a, const void* b, int M, int N, int K, float alpha, const uint16_t* sa,
-                const uint16_t* sb, void* out, int64_t ldo, cudaStream_t stream) {
+                const uint16_t* sb, void* out, int64_t ldo, cudaStream_t stream, const EpiQ& q = EpiQ{},
+                const void* b2 = nullptr) {
     if (M > BM && pair_mode() == 2)
-        return run_cta<kF8, kAMN, kBMN, kOutBf16, 2>(a, b, M, N, K, alpha, sa, sb, out, ldo, stream);
-    return run_cta<kF8, kAMN, kBMN, kOutBf16, 1>(a, b, M, N, K, alpha, sa, sb, out, ldo, stream);
+        return run_cta<kF8, kAMN, kBMN, kOut, 2>(a, b, b2, M, N, K, alpha, sa, sb, out, ldo, q, stream);
+    return run_cta<kF8, kAMN, kBMN, kOut, 1>(a, b, b2, M, N, K, alpha, sa, sb, out, ldo, q, stream);
 }
 
 }  // namespace gemm
@@ -528,17 +669,51 @@ cudaError_t run(const void* a, const void* b, int M, int N, int K, float alpha, 
 // y[M,N] (fp32) = (s_x s_w) * codes_x[M,K] . codes_w[K,N]   (W row-major (K,N): MN-major B)
 cudaError_t launch_fp8_linear_fwd(const uint8_t* xc, const uint16_t* sx, const uint8_t* wc, const uint16_t* sw, int M,
                                   int K, int N, float* y, cudaStream_t st) {
-    return gemm::run<true, false, true, false>(xc, wc, M, N, K, 1.0f, sx, sw, y, N, st);
+    return gemm::run<true, false, true, gemm::kOutF32>(xc, wc, M, N, K, 1.0f, sx, sw, y, N, st);
+}
+// The same y quantized per group of 16 in the epilogue (y never reaches HBM
+// unless y_out is given).
+cudaError_t launch_fp8_linear_fwd_q16(const uint8_t* xc, const uint16_t* sx, const uint8_t* wc, const uint16_t* sw,
+                                      int M, int K, int N, uint8_t* y_codes, uint16_t* y_scales, float* y_out,
+                                      uint32_t* flags, cudaStream_t st) {
+    gemm::EpiQ q{};
+    q.c0 = y_codes;
+    q.s0 = y_scales;
+    q.y0 = y_out;
+    q.flags = flags;
+    q.ldc = N;
+    return gemm::run<true, false, true, gemm::kOutQ16>(xc, wc, M, N, K, 1.0f, sx, sw, nullptr, N, st, q);
+}
+// The gate/up projections of the Llama MLP in one GEMM with the SiLU*mul
+// block's quantizers in the epilogue; the per-tensor down.in encode follows
+// from the codes (silu_mul pass 2).
+cudaError_t launch_fp8_upgate_silu(const UpGateArgs& a, cudaStream_t st) {
+    gemm::EpiQ q{};
+    q.c0 = a.gcodes; q.s0 = a.gscales;
+    q.c1 = a.scodes; q.s1 = a.sscales;
+    q.c2 = a.ucodes; q.s2 = a.uscales;
+    q.y0 = a.gate_out; q.y1 = a.up_out;
+    q.scale_b1 = a.s_wu;
+    q.amax_bits = a.amax_bits;
+    q.flags = a.flags;
+    q.ldc = a.I;
+    cudaError_t e = cudaMemsetAsync(a.amax_bits, 0, 4, st);
+    if (e != cudaSuccess) return e;
+    e = gemm::run<true, false, true, gemm::kOutUpGate>(a.xc, a.wg, int(a.M), int(a.I), int(a.H), 1.0f, a.sx, a.s_wg,
+                                                        nullptr, a.I, st, q, a.wu);
+    if (e != cudaSuccess) return e;
+    return launch_silu_mul_pass2(a.scodes, a.sscales, a.ucodes, a.uscales, a.M * a.I, a.amax_bits, a.pcodes, a.pscale,
+                                 a.pout, a.flags, st);
 }
 // dX[M,K] (bf16) = s_w * dY[M,N] . Wd[K,N]^T    (Wd = decoded W codes in bf16, exact; B K-major)
 cudaError_t launch_linear_dgrad(const uint16_t* dy, const uint16_t* wd, const uint16_t* sw, int M, int K, int N,
                                 uint16_t* dx, cudaStream_t st) {
-    return gemm::run<false, false, false, true>(dy, wd, M, K, N, 1.0f, sw, nullptr, dx, K, st);
+    return gemm::run<false, false, false, gemm::kOutBf16>(dy, wd, M, K, N, 1.0f, sw, nullptr, dx, K, st);
 }
 // dW[K,N] (fp32) = s_x * Xd[M,K]^T . dY[M,N]     (A = Xd MN-major, B = dY MN-major)
 cudaError_t launch_linear_wgrad(const uint16_t* xd, const uint16_t* sx, const uint16_t* dy, int M, int K, int N,
                                 float* dw, cudaStream_t st) {
-    return gemm::run<false, true, true, false>(xd, dy, K, N, M, 1.0f, sx, nullptr, dw, N, st);
+    return gemm::run<false, true, true, gemm::kOutF32>(xd, dy, K, N, M, 1.0f, sx, nullptr, dw, N, st);
 }
 
 }  // namespace coat

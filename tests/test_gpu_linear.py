@@ -107,3 +107,77 @@ def test_linear_errors(coat):
     qg = coat.quantize(torch.randn(128, 256, device="cuda"), coat.QuantGeometry.per_group(16))
     with pytest.raises(coat.InvalidSpec):
         coat.fp8_linear(qg, qw)
+
+
+# ------------------------------------------------ quantizing GEMM epilogues ----
+# SURVEY.md 8(f)#2 / PAPER.md:661-662: the per-group (1x16) quantizer of a GEMM
+# output runs in the tcgen05 epilogue.  Parity: the codes and scales equal the
+# oracle's quantize(y, 16) (quantize.cpp:89-111) applied to the kernel's own
+# fp32 y, which the epilogue optionally writes beside them and which must be
+# bit-identical to the plain forward GEMM's output.
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("M,K,N", [(128, 256, 256), (200, 272, 400), (512, 1024, 768), (8192, 4096, 11008)])
+def test_fp8_linear_q16_epilogue(coat, port, M, K, N):
+    import torch
+    qx, qw = _quant_pair(coat, M, K, N, seed=M + 3 * N)
+    y_ref = coat.fp8_linear(qx, qw)
+    q, y = coat.fp8_linear_q16(qx, qw, return_y=True)
+    q_only = coat.fp8_linear_q16(qx, qw)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32), y_ref.view(torch.int32)), "epilogue y differs from the forward GEMM"
+    assert torch.equal(q.codes, q_only.codes) and torch.equal(q.scales, q_only.scales)
+    rows = slice(None) if M * N <= (1 << 22) else slice(0, 256)   # the oracle on a row sample at full size
+    yh = _np(y)[rows]
+    codes, scales = port.quantize(yh, 16)
+    assert np.array_equal(_np(q.codes)[rows], codes)
+    assert np.array_equal(_np(q.scales.float()).reshape(M, N // 16)[rows].ravel(), scales)
+    qd = coat.quantize(y, coat.QuantGeometry.per_group(16))   # the standalone device quantizer, every row
+    assert torch.equal(q.codes, qd.codes) and torch.equal(q.scales, qd.scales)
+
+
+@pytest.mark.parametrize("M,H,I", [(128, 256, 256), (200, 272, 400), (384, 512, 1040), (8192, 4096, 11008)])
+def test_fp8_upgate_silu_epilogue(coat, port, M, H, I):
+    """The fused gate/up GEMM + SiLU*mul quantizers == the two forward GEMMs
+    followed by the SiLU*mul block (itself checked against the reference's
+    DecoderLayer tape in test_gpu_producers.py), bit for bit; silu.in and
+    mul.in.up also against the oracle's quantize on the GEMM outputs."""
+    import torch
+    qx, qwg = _quant_pair(coat, M, H, I, seed=7 * M + I)
+    _, qwu = _quant_pair(coat, M, H, I, seed=7 * M + I + 1)
+    gate = coat.fp8_linear(qx, qwg)
+    up = coat.fp8_linear(qx, qwu)
+    ref = coat.silu_mul_quantize(gate, up, return_prod=True)
+    out = coat.fp8_upgate_silu(qx, qwg, qwu, return_fp32=True)
+    fused = coat.fp8_upgate_silu(qx, qwg, qwu)
+    torch.cuda.synchronize()
+    g, u, p = out[4], out[5], out[6]
+    assert torch.equal(g.view(torch.int32), gate.view(torch.int32))
+    assert torch.equal(u.view(torch.int32), up.view(torch.int32))
+    for a, b, c in zip(out[:4], ref[:4], fused):
+        assert torch.equal(a.codes, b.codes) and torch.equal(a.scales, b.scales)
+        assert torch.equal(c.codes, b.codes) and torch.equal(c.scales, b.scales)
+    assert torch.equal(p.view(torch.int32), ref[4].view(torch.int32))
+    rows = slice(None) if M * I <= (1 << 22) else slice(0, 128)
+    for rec, src in ((out[0], gate), (out[2], up)):
+        codes, scales = port.quantize(_np(src)[rows], 16)
+        assert np.array_equal(_np(rec.codes)[rows], codes)
+        assert np.array_equal(_np(rec.scales.float()).reshape(M, I // 16)[rows].ravel(), scales)
+
+
+def test_quantizing_epilogue_nonfinite(coat):
+    """A NaN code in x (E4M3 0x7F) makes y non-finite: quantize throws
+    NonFiniteInput (quantize.cpp:91), so both epilogues raise it."""
+    import torch
+    qx, qw = _quant_pair(coat, 256, 256, 256, seed=3)
+    qx.codes[17, 5] = 0x7F
+    with pytest.raises(coat.NonFiniteInput):
+        coat.fp8_linear_q16(qx, qw)
+    with pytest.raises(coat.NonFiniteInput):
+        coat.fp8_upgate_silu(qx, qw, qw)
+    with pytest.raises(coat.GeometryMismatch):
+        qa, qb = _quant_pair(coat, 128, 256, 264, seed=4)   # N % 16 != 0 is rejected
+        coat.fp8_linear_q16(qa, qb)
