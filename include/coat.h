@@ -239,6 +239,31 @@ coat_status coat_zero_step(float* w_full, const float* g_full, int64_t n_total, 
                            coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t, float* g_shard,
                            float* w_scratch, uint32_t* d_flags, void* nccl_comm, int32_t rank, int32_t nranks,
                            void* stream);
+/* The same ZeRO step with the collectives done by SM kernels over NVLink peer
+ * memory instead of NCCL, pipelined chunk by chunk with the
+ * fused step so the reduce and the broadcast overlap it:
+ *   g_shard = sum over ranks r of rank r's gradient slice [rank*n, (rank+1)*n),
+ *     read in place: from g_peers[r] (P2P pointers, summed in rank order
+ *     r = 0, 1, ..., fp32 or bf16 wire (g_dtype 0 / 1, exact widening)) or,
+ *     when g_mc (a multicast address over the fp32 gradient buffers) is
+ *     given, by NVLink SHARP multimem.ld_reduce;
+ *   w_next[shard] = the fused step of w_cur[shard] (coat_adamw_dre_step);
+ *   every rank's next-weight buffer receives the shard: P2P stores into
+ *     w_next_peers[r] (r != rank), or multimem.st into w_next_mc.
+ * n = n_total / nranks as for coat_zero_step; w_cur / w_next are this rank's
+ * full buffers (double-buffered: nothing the step reads is overwritten).
+ * Stream-ordered; the caller synchronizes the ranks (e.g. an all-reduce of the
+ * error word) before reading w_next or rewriting its gradients, then commits
+ * m_out, v_out and w_next -- or keeps w_cur and the old state -- by the OR of
+ * every rank's *d_flags (coat_flags_to_status), exactly as the reference's
+ * step commits or throws as a whole (optimizer.cpp:101-114).  chunk <= 0:
+ * 64 Mi parameters.  nranks <= 16. */
+coat_status coat_zero_step_p2p(const void* const* g_peers, const void* g_mc, int32_t g_dtype,
+                               float* const* w_next_peers, float* w_next_mc, const float* w_cur, float* w_next,
+                               int64_t n_total, int64_t group_size, coat_moment_state m_in,
+                               coat_moment_state v_in, coat_moment_state m_out, coat_moment_state v_out,
+                               const coat_adamw_config* cfg, int64_t t, float* g_shard, uint32_t* d_flags,
+                               int32_t rank, int32_t nranks, int64_t chunk, void* stream);
 /* Communicator helpers for callers without their own NCCL binding: rank 0
  * creates the 128-byte id, every rank passes it to coat_nccl_comm_init. */
 coat_status coat_nccl_unique_id(uint8_t* out_id /* 128 bytes */);

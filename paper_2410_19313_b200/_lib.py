@@ -62,6 +62,8 @@ _SIGS = {
     "coat_last_error": ([], C.c_char_p),
     "coat_zero_step": ([_vp, _vp, _i64, _i64, MomentState, MomentState, MomentState, MomentState, _vp, _i64,
                         _vp, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp], _int),
+    "coat_zero_step_p2p": ([_vp, _vp, C.c_int32, _vp, _vp, _vp, _vp, _i64, _i64, MomentState, MomentState,
+                            MomentState, MomentState, _vp, _i64, _vp, _vp, C.c_int32, C.c_int32, _i64, _vp], _int),
     "coat_nccl_unique_id": ([_vp], _int),
     "coat_nccl_comm_init": ([_vp, C.c_int32, _vp, C.c_int32], _int),
     "coat_nccl_comm_destroy": ([_vp], _int),
@@ -69,6 +71,7 @@ _SIGS = {
     "coat_test_pack_prepare": ([_vp, _vp, _i64, C.c_double, _vp, _vp], _int),
     "coat_test_expf_neg2": ([C.c_uint64, C.c_uint64, _vp, _vp], _int),
     "coat_test_k1_layout": ([], _int),
+    "coat_test_mufu_bounds": ([C.c_float, C.c_float, C.c_float, _vp, _vp], _int),
     "coat_flags_to_status": ([C.c_uint32], _int),
     "coat_device_sm_count": ([], _int),
     "coat_encode_e4m3": ([_vp, _vp, _i64, _vp, _vp], _int),

@@ -381,6 +381,45 @@ coat_status coat_zero_step(float* w_full, const float* g_full, int64_t n_total, 
     return nccl_status(zero_all_gather(w_scratch, w_full, n, comm, s), "ncclAllGather");
 }
 
+coat_status coat_zero_step_p2p(const void* const* g_peers, const void* g_mc, int32_t g_dtype,
+                               float* const* w_next_peers, float* w_next_mc, const float* w_cur, float* w_next,
+                               int64_t n_total, int64_t G, coat_moment_state m_in, coat_moment_state v_in,
+                               coat_moment_state m_out, coat_moment_state v_out, const coat_adamw_config* cfg,
+                               int64_t t, float* g_shard, uint32_t* d_flags, int32_t rank, int32_t nranks,
+                               int64_t chunk, void* stream) {
+    if (nranks < 1 || nranks > 16 || rank < 0 || rank >= nranks)
+        return fail(COAT_ERR_INVALID, "zero_step_p2p: bad rank / nranks (1..16)");
+    if (!w_cur || !w_next || !g_shard || !d_flags) return fail(COAT_ERR_INVALID, "zero_step_p2p: NULL buffer");
+    if (!g_mc && !g_peers) return fail(COAT_ERR_INVALID, "zero_step_p2p: gradients need g_peers or g_mc");
+    if (!w_next_mc && !w_next_peers && nranks > 1)
+        return fail(COAT_ERR_INVALID, "zero_step_p2p: weights need w_next_peers or w_next_mc");
+    if (g_dtype != 0 && g_dtype != 1) return fail(COAT_ERR_INVALID, "zero_step_p2p: g_dtype 0 (fp32) or 1 (bf16)");
+    if (g_mc && g_dtype != 0) return fail(COAT_ERR_INVALID, "zero_step_p2p: the multimem reduce is fp32");
+    if (n_total <= 0 || n_total % (128 * int64_t(nranks)) != 0)
+        return fail(COAT_ERR_GEOMETRY, "zero_step_p2p: n_total must be a positive multiple of 128 * nranks");
+    uintptr_t al = reinterpret_cast<uintptr_t>(w_cur) | reinterpret_cast<uintptr_t>(w_next) |
+                   reinterpret_cast<uintptr_t>(g_shard) | reinterpret_cast<uintptr_t>(g_mc) |
+                   reinterpret_cast<uintptr_t>(w_next_mc);
+    for (int r = 0; r < nranks; ++r) {
+        if (g_peers) {
+            if (!g_peers[r]) return fail(COAT_ERR_INVALID, "zero_step_p2p: NULL gradient peer");
+            al |= reinterpret_cast<uintptr_t>(g_peers[r]);
+        }
+        if (w_next_peers) {
+            if (!w_next_peers[r]) return fail(COAT_ERR_INVALID, "zero_step_p2p: NULL weight peer");
+            al |= reinterpret_cast<uintptr_t>(w_next_peers[r]);
+        }
+    }
+    if (al & 15u) return fail(COAT_ERR_INVALID, "zero_step_p2p: buffers must be 16-byte aligned");
+    const int64_t n = n_total / nranks;
+    AdamWScalars a;
+    const coat_status st = step_args(cfg, n, G, t, m_in, v_in, m_out, v_out, a);
+    if (st != COAT_OK) return st;
+    ZeroP2PArgs z{g_peers, g_mc, int(g_dtype), w_next_peers, w_next_mc, w_cur, w_next, n, m_in, v_in, m_out,
+                  v_out, g_shard, int(rank), int(nranks), chunk};
+    return cuda_status(zero_p2p_step(z, a, d_flags, g_fallback_counter, S(stream)));
+}
+
 coat_status coat_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n, int64_t G,
                                 coat_moment_state m_in, coat_moment_state v_in, coat_moment_state m_out,
                                 coat_moment_state v_out, const coat_adamw_config* cfg, int64_t t,

@@ -53,6 +53,26 @@ cudaError_t launch_make_slot(const MomentStateOut& st, int64_t npad, cudaStream_
 
 // host_pipeline.cu: host-resident w/g streamed through K1 (state in HBM)
 }  // namespace coat
+#include "../../include/coat.h"
+namespace coat {
+// zero_p2p.cu: the ZeRO step with peer-memory (P2P / NVLink SHARP) collectives
+struct ZeroP2PArgs {
+    const void* const* g_peers;   // [nranks] every rank's full gradient buffer (fp32 / bf16), or NULL with g_mc
+    const void* g_mc;             // multicast address of the gradient buffers (fp32), or NULL
+    int g_dtype;                  // 0 fp32, 1 bf16 (P2P only)
+    float* const* w_next_peers;   // [nranks] every rank's next-weight buffer, or NULL with w_next_mc
+    float* w_next_mc;             // multicast address of the next-weight buffers, or NULL
+    const float* w_cur;           // this rank's full current weights
+    float* w_next;                // this rank's full next-weight buffer
+    int64_t n_shard;
+    coat_moment_state m_in, v_in, m_out, v_out;
+    float* g_shard;               // n_shard floats of scratch: the reduced gradient shard
+    int rank, nranks;
+    int64_t chunk;
+};
+cudaError_t zero_p2p_step(const ZeroP2PArgs& z, const AdamWScalars& a, uint32_t* flags,
+                          unsigned long long* fallbacks, cudaStream_t stream);
+}  // namespace coat
 #include <string>
 #include "../../include/coat.h"
 namespace coat {

@@ -11,9 +11,16 @@
 // CUDA's scalar expf(-x) over every float bit pattern in [first, first+count);
 // *mismatches counts the bitwise differences.
 //
+// coat_test_mufu_bounds: exhaustive error of the SFU approximations behind the
+// certified expand of the DRE pack (dre.cuh kRelMufu):
+// max |lg2.approx.ftz(r) - log2(r)| / (1 + |log2 r|) over every float r in
+// [lo_r, hi_r) (an absolute plus a relative part) and max |ex2.approx.ftz(u) /
+// 2^u - 1| over every float u with |u| < hi_u, against double log2 / exp2.
+//
 // coat_test_k1_layout: element warps per CTA of the K1 layout this process
 // selected (COAT_K1_EW; tests/test_gpu_k1_layouts.py).
 #include <cstdint>
+#include <cstring>
 
 #include "coat_device.cuh"
 #include "coat_internal.h"
@@ -59,8 +66,41 @@ __global__ void __launch_bounds__(256) expf_neg2_check_kernel(uint64_t first, ui
     if (bad) atomicAdd(mismatches, bad);
 }
 
+__device__ __forceinline__ void atomic_max_nonneg_double(unsigned long long* dst, double v) {
+    atomicMax(dst, (unsigned long long)__double_as_longlong(v));   // v >= 0: bit order = value order
+}
+
+__global__ void __launch_bounds__(256) mufu_bounds_kernel(uint32_t r0, uint32_t r1, uint32_t u0, uint32_t u1,
+                                                          unsigned long long* out) {
+    double e_lg = 0.0, e_ex = 0.0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t b = r0 + blockIdx.x * blockDim.x + threadIdx.x; b < r1; b += stride) {
+        const float r = u2f(b);
+        const double l = log2((double)r);
+        e_lg = fmax(e_lg, fabs((double)dre::lg2_approx(r) - l) / (1.0 + fabs(l)));
+    }
+    // u in [lo_u, hi_u): positive bit patterns [u0, u1) and their negations
+    for (uint32_t b = u0 + blockIdx.x * blockDim.x + threadIdx.x; b < u1; b += stride) {
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg) {
+            const float u = u2f(b | (sg ? 0x80000000u : 0u));
+            e_ex = fmax(e_ex, fabs((double)dre::ex2_approx(u) / exp2((double)u) - 1.0));
+        }
+    }
+    atomic_max_nonneg_double(&out[0], e_lg);
+    atomic_max_nonneg_double(&out[1], e_ex);
+}
+
 }  // namespace
 }  // namespace coat
+
+extern "C" int coat_test_mufu_bounds(float lo_r, float hi_r, float hi_u, unsigned long long* out, void* stream) {
+    uint32_t b[3];
+    const float f[3] = {lo_r, hi_r, hi_u};
+    memcpy(b, f, sizeof(b));
+    coat::mufu_bounds_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(b[0], b[1], 0u, b[2], out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
 
 extern "C" int coat_test_pack_prepare(const uint32_t* lo, const uint32_t* hi, int64_t n, double log_target, float* out,
                                       void* stream) {

@@ -97,3 +97,25 @@ def test_special_extrema():
     lo += [np.uint32(0x3F800000), np.uint32(0x00000001), np.uint32(0x3F800000)]
     hi += [np.uint32(0x7F800000), np.uint32(0x7FC00000), np.uint32(0x7F7FFFFF)]   # Inf, NaN, FLT_MAX
     _check(np.array(lo, dtype=np.uint32), np.array(hi, dtype=np.uint32))
+
+
+def test_mufu_error_bounds():
+    """The error model behind the DRE pack's flat 2^-15 certification interval
+    (dre.cuh kRelMufu; k1_ws.cu pack4_sfu), exhaustively on this hardware:
+    lg2.approx.ftz(r) is within 2^-22 * (1 + |log2 r|) of log2(r) for every
+    float r in [2^-10, 2^10] (r = |x| * RN(1/c): |x|/c in [2^-9, 2^9] by
+    measure_group), and ex2.approx.ftz(u) within 2^-22 (relative) of 2^u for
+    every float |u| < 9.5 (|u| = |k log2(|x|/c)| <= 8.95).  Then q = RN(RN(ex2(
+    RN(k * lg2(RN(|x| RN(1/c)))))) RN(1/s)) has relative error <= ln2 * (k *
+    2^-22 + 8.95 * 2^-22 + 8.95 * 2^-24) + k * 2^-23 + 2^-22 + 2^-23 < 2^-16.9
+    for k <= 20: the interval keeps a 3.7x margin."""
+    import torch
+    from paper_2410_19313_b200 import _lib
+    out = torch.zeros(2, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert _lib.lib.coat_test_mufu_bounds(2.0 ** -10, 2.0 ** 10, 9.5, out.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    e_lg, e_ex = out.cpu().numpy().view(np.float64)
+    print(f"lg2.approx max err / (1 + |log2 r|) 2^{math.log2(e_lg):.2f}, ex2.approx max rel err "
+          f"2^{math.log2(e_ex):.2f}")
+    assert e_lg <= 2.0 ** -22 and e_ex <= 2.0 ** -22

@@ -1,0 +1,157 @@
+"""GPU: the ZeRO step with peer-memory collectives (coat_zero_step_p2p,
+SURVEY.md 8(f)#3): reduce-scatter by direct loads from every rank's gradient
+buffer, the fused step on the shard, all-gather by direct stores into every
+rank's next-weight buffer, pipelined chunk by chunk.
+
+One GPU is available, so N ranks are N "virtual ranks" on the same device:
+each owns its own full gradient, current-weight and next-weight buffers and
+its shard's optimizer state, and the peer pointer arrays point at the other
+virtual ranks' buffers -- the same kernels and pipeline a multi-GPU node runs,
+with NVLink replaced by local HBM.  Parity: the reduced gradient is the
+rank-order fp32 sum (bf16 wire: of the exactly widened values), and the
+gathered weights and every shard's state equal the checker's step of the whole
+tensor on that sum (groups are independent, so sharded == whole,
+SPEC.md:396), against both the C restatement and the reference itself.
+The NVLink-SHARP (multimem) branch needs a multicast object, which a one-GPU
+box cannot create (tools/mc_probe.py); it shares this pipeline and differs
+only in the two copy kernels.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import rng
+
+pytestmark = pytest.mark.gpu
+
+CFG = {"beta1": 0.9, "beta2": 0.999, "lr": 1e-3, "weight_decay": 0.1, "eps": 1e-8}
+
+
+def _moment(n, torch):
+    ng = n // 128
+    return {"codes": torch.zeros(n, dtype=torch.uint8, device="cuda"),
+            "scales": torch.full((ng,), 0x3B00, dtype=torch.int16, device="cuda"),   # 2^-9 (make_slot)
+            "k": torch.ones(ng, device="cuda"), "c": torch.ones(ng, device="cuda")}
+
+
+def _cs(_lib, mm):
+    return _lib.MomentState(mm["codes"].data_ptr(), mm["scales"].data_ptr(), mm["k"].data_ptr(), mm["c"].data_ptr())
+
+
+def _ptrs(ts):
+    return (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+
+def _bf16_round(x):
+    b = x.view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) >> 16
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.parametrize("nranks,wire", [(1, "fp32"), (2, "fp32"), (4, "fp32"), (3, "bf16"), (8, "bf16")])
+def test_p2p_step_virtual_ranks(checker, nranks, wire):
+    import torch
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    n = 128 * 2100 + 128 * 7            # per-rank shard: ragged against the 2048-parameter round
+    N = n * nranks
+    r = rng(100 + nranks)
+    w0 = (r.standard_normal(N) * 0.02).astype(np.float32)
+    cfg = _lib.AdamWConfigC(**CFG)
+    st = torch.cuda.current_stream().cuda_stream
+    w_cur = [torch.from_numpy(w0).cuda() for _ in range(nranks)]
+    w_next = [torch.full((N,), float("nan"), device="cuda") for _ in range(nranks)]
+    m = [[_moment(n, torch), _moment(n, torch)] for _ in range(nranks)]
+    v = [[_moment(n, torch), _moment(n, torch)] for _ in range(nranks)]
+    g_shard = [torch.empty(n, device="cuda") for _ in range(nranks)]
+    flags = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(nranks)]
+    w_ref = w0.copy()
+    mr, vr = checker.make_slot(N)
+    for t in range(1, 4):
+        gh = [(r.standard_normal(N) * 1e-3).astype(np.float32) for _ in range(nranks)]
+        if wire == "bf16":
+            gh = [_bf16_round(x) for x in gh]
+            g = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in gh]
+        else:
+            g = [torch.from_numpy(x).cuda() for x in gh]
+        gsum = gh[0].copy()
+        for x in gh[1:]:
+            gsum = (gsum + x).astype(np.float32)    # rank order, fp32 RN
+        a, b = (t - 1) % 2, t % 2
+        for rk in range(nranks):
+            flags[rk].zero_()
+            assert L.coat_zero_step_p2p(_ptrs(g), None, 0 if wire == "fp32" else 1, _ptrs(w_next), None,
+                                        w_cur[rk].data_ptr(), w_next[rk].data_ptr(), N, 128,
+                                        _cs(_lib, m[rk][a]), _cs(_lib, v[rk][a]), _cs(_lib, m[rk][b]),
+                                        _cs(_lib, v[rk][b]), C.byref(cfg), t, g_shard[rk].data_ptr(),
+                                        flags[rk].data_ptr(), rk, nranks, 2048 * 5, st) == 0, L.coat_last_error()
+        torch.cuda.synchronize()
+        assert all(int(f.item()) == 0 for f in flags)
+        assert checker.step(w_ref, gsum, mr, vr, t - 1, CFG) == 0
+        for rk in range(nranks):
+            assert np.array_equal(g_shard[rk].cpu().numpy().view(np.uint32),
+                                  gsum[rk * n:(rk + 1) * n].view(np.uint32)), (t, rk, "reduced gradient")
+            assert np.array_equal(w_next[rk].cpu().numpy().view(np.uint32), w_ref.view(np.uint32)), (t, rk)
+            sl = slice(rk * n, (rk + 1) * n)
+            gs = slice(rk * n // 128, (rk + 1) * n // 128)
+            for mine, full in ((m[rk][b], mr), (v[rk][b], vr)):
+                assert np.array_equal(mine["codes"].cpu().numpy(), full["codes"][sl]), (t, rk)
+                assert np.array_equal(mine["scales"].cpu().numpy().view(np.uint16).astype(np.uint32) << 16,
+                                      full["scales"][gs].view(np.uint32)), (t, rk)
+                assert np.array_equal(mine["k"].cpu().numpy(), full["k"][gs])
+                assert np.array_equal(mine["c"].cpu().numpy(), full["c"][gs])
+        w_cur, w_next = w_next, w_cur            # commit: the next weights become current
+
+
+def test_p2p_step_nonfinite_gradient_leaves_current_weights(coat):
+    """A NaN in one rank's gradient reaches the shard owner's reduced sum: its
+    error word reports NonFiniteGradient (optimizer.cpp:104) and, the weights
+    being double-buffered, every rank's current weights are untouched -- the
+    caller keeps them by the OR of the error words."""
+    import torch
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    nranks, n = 2, 128 * 1024
+    N = n * nranks
+    r = rng(7)
+    w0 = torch.from_numpy((r.standard_normal(N) * 0.02).astype(np.float32)).cuda()
+    w_cur = [w0.clone() for _ in range(nranks)]
+    w_next = [torch.empty(N, device="cuda") for _ in range(nranks)]
+    g = [torch.from_numpy((r.standard_normal(N) * 1e-3).astype(np.float32)).cuda() for _ in range(nranks)]
+    g[0][n + 77] = float("nan")                  # rank 0's gradient, inside rank 1's shard
+    cfg = _lib.AdamWConfigC(**CFG)
+    st = torch.cuda.current_stream().cuda_stream
+    fl = []
+    for rk in range(nranks):
+        m, v = [_moment(n, torch), _moment(n, torch)], [_moment(n, torch), _moment(n, torch)]
+        f = torch.zeros(1, dtype=torch.int32, device="cuda")
+        gs = torch.empty(n, device="cuda")
+        assert L.coat_zero_step_p2p(_ptrs(g), None, 0, _ptrs(w_next), None, w_cur[rk].data_ptr(),
+                                    w_next[rk].data_ptr(), N, 128, _cs(_lib, m[0]), _cs(_lib, v[0]),
+                                    _cs(_lib, m[1]), _cs(_lib, v[1]), C.byref(cfg), 1, gs.data_ptr(), f.data_ptr(),
+                                    rk, nranks, 0, st) == 0
+        fl.append(f)
+    torch.cuda.synchronize()
+    word = int(fl[0].item()) | int(fl[1].item())
+    assert int(fl[1].item()) & _lib.FLAG_NONFINITE_GRAD and not int(fl[0].item()) & _lib.FLAG_NONFINITE_GRAD
+    assert L.coat_flags_to_status(word) == 4     # NonFiniteGradient for every rank after the OR
+    assert all(torch.equal(w, w0) for w in w_cur)
+
+
+def test_p2p_step_validates_before_any_work():
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    cfg = _lib.AdamWConfigC(**CFG)
+    ms = _lib.MomentState(None, None, None, None)
+    one = (C.c_void_p * 1)(16)
+    # n_total not a multiple of 128 * nranks -> GeometryMismatch
+    assert L.coat_zero_step_p2p(one, None, 0, one, None, 16, 16, 1000, 128, ms, ms, ms, ms, C.byref(cfg), 1, 16,
+                                16, 0, 1, 0, None) == 2
+    # bad rank, 17 ranks, multimem with bf16
+    assert L.coat_zero_step_p2p(one, None, 0, one, None, 16, 16, 1024, 128, ms, ms, ms, ms, C.byref(cfg), 1, 16,
+                                16, 1, 1, 0, None) == 5
+    assert L.coat_zero_step_p2p(one, None, 0, one, None, 16, 16, 1024 * 17, 128, ms, ms, ms, ms, C.byref(cfg), 1,
+                                16, 16, 0, 17, 0, None) == 5
+    assert L.coat_zero_step_p2p(None, 16, 1, one, None, 16, 16, 1024, 128, ms, ms, ms, ms, C.byref(cfg), 1, 16,
+                                16, 0, 1, 0, None) == 5
