@@ -472,6 +472,21 @@ def run_adamw(args):
             out["k1_only"] = {"ms_per_step": ms_k1, "kernel_ms": k_ms, "value": P / (ms_k1 * 1e-3),
                               "unit": "params/s", "clocks": clocks_k1,
                               "note": "K1 on every rank's shard, no collectives (max over ranks)"}
+    # ---- N > 1: the same ZeRO step with the collectives as peer-memory kernels
+    # (coat_zero_step_p2p over torch symmetric memory; NVLink SHARP when the
+    # platform gives a multicast address) -- a side measurement, so a platform
+    # without it keeps the NCCL line above
+    if ws > 1 and os.environ.get("COAT_BENCH_P2P", "1") != "0":
+        w_full = g_full = w_scratch = None          # the NCCL path's buffers make room
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        try:
+            p2p = run_zero_p2p(args, L, _lib, P, n, ws, rank, m, v, cur, t_step, cfg, flags, g_shard, stream,
+                               dev, timed)
+        except Exception as ex:
+            p2p = {"error": repr(ex)[:300]}
+        if rank == 0:
+            out["zero_p2p"] = p2p
     if comm is not None:
         torch.cuda.synchronize()
         L.coat_nccl_comm_destroy(comm)
@@ -492,6 +507,68 @@ def run_adamw(args):
             torch.cuda.empty_cache()
         out["extra"] = extra
     print(json.dumps(out))
+
+
+def run_zero_p2p(args, L, _lib, P, n, ws, rank, m, v, cur, t_step, cfg, flags, g_shard, stream, dev, timed):
+    """The ZeRO step of zero.PeerZeroAdamW on P parameters: symmetric-memory
+    gradient (fp32) and double-buffered weights; per step a device barrier over
+    the ranks, coat_zero_step_p2p (peer-load reduce-scatter or multimem, K1,
+    peer-store / multicast all-gather, chunk-pipelined) and the device-side OR
+    of the error words (NCCL all_reduce of the flag lanes)."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    free, _ = torch.cuda.mem_get_info()
+    need = 3 * 4 * P
+    if need > free * 0.95:
+        return {"unavailable": f"needs {need / 1e9:.1f} GB of symmetric memory per rank, {free / 1e9:.1f} GB free"}
+    gb = symm_mem.empty(P, dtype=torch.float32, device=dev)
+    wb = [symm_mem.empty(P, dtype=torch.float32, device=dev) for _ in range(2)]
+    name = dist.group.WORLD.group_name
+    hg = symm_mem.rendezvous(gb, name)
+    hw = [symm_mem.rendezvous(x, name) for x in wb]
+    Ptr = C.c_void_p * ws
+    g_peers = Ptr(*hg.buffer_ptrs)
+    w_peers = [Ptr(*h.buffer_ptrs) for h in hw]
+    g_mc = hg.multicast_ptr or None
+    w_mc = [h.multicast_ptr or None for h in hw]
+    gen = torch.Generator(device=dev).manual_seed(4321)
+    _fill_synthetic(torch, wb[0], gb, gen)          # identical weights on every rank (same seed) ...
+    gb.mul_(1.0 + 0.001 * rank)                     # ... rank-specific gradients
+    bits = torch.zeros(8, dtype=torch.int32, device=dev)
+    wc = [0]
+    gloo = dist.get_backend() == "gloo"
+
+    def step():
+        i, j = cur[0], 1 - cur[0]
+        t_step[0] += 1
+        hg.barrier()
+        s = L.coat_zero_step_p2p(g_peers, g_mc, 0, w_peers[1 - wc[0]], w_mc[1 - wc[0]], wb[wc[0]].data_ptr(),
+                                 wb[1 - wc[0]].data_ptr(), P, GROUP, _cstate(_lib, m[i]), _cstate(_lib, v[i]),
+                                 _cstate(_lib, m[j]), _cstate(_lib, v[j]), C.byref(cfg), t_step[0],
+                                 g_shard.data_ptr(), flags.data_ptr(), rank, ws, 0, stream.cuda_stream)
+        if s != 0:
+            raise RuntimeError(L.coat_last_error())
+        for b in range(8):                           # the error word as MAX-reduced lanes (= OR)
+            bits[b] = (flags[0] >> b) & 1
+        if gloo:
+            hb = bits.cpu()
+            dist.all_reduce(hb, op=dist.ReduceOp.MAX)
+            bits.copy_(hb)
+        else:
+            dist.all_reduce(bits, op=dist.ReduceOp.MAX)
+        cur[0] = j
+        wc[0] = 1 - wc[0]
+
+    for _ in range(max(2, args.warmup)):
+        step()
+    ms, _, clocks = timed(step, args.steps)
+    assert int(bits.sum().item()) == 0 and int(flags.item()) == 0
+    return {"value": P / (ms * 1e-3), "unit": "params/s", "ms_per_step": ms, "clocks": clocks,
+            "collectives": "NVLink SHARP multimem.ld_reduce / multimem.st" if g_mc else "P2P peer loads / stores",
+            "wire": "fp32", "step": "symmetric-memory barrier -> coat_zero_step_p2p (reduce-scatter, K1, all-gather "
+                                   "pipelined in 64 Mi-param chunks) -> error-word all_reduce"}
 
 
 def run_e2e(args, L, _lib, P, n, ws, rank, w, g, w_full, g_full, g_shard, w_scratch, m, v, cur, t_step, cfg,
@@ -731,12 +808,23 @@ def run_mgaq(args, extra_mode=False):
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     nel = sum(r * c for _, r, c, *_ in bufs)
 
+    def branch_of(i):
+        """Records round-robin over the branches (as coat_quantize_batch's
+        streams).  Measured round 2: the per-tensor records all on one branch
+        (one L2-resident tensor at a time) cut the DRAM traffic from 1.17x to
+        1.12x the algorithmic bytes but serialise 8 short kernels: 0.330 vs
+        0.318 ms."""
+        return i % nbr
+
+    nbr = max(1, args.mgaq_branches)
+
     def step(record=None, streams=None):
-        """The nine records; with `streams`, record i goes to streams[i % K]
-        (independent records overlap one kernel's tail with the next's ramp)."""
+        """The nine records; with `streams`, record i goes to
+        streams[branch_of(i)] (independent records overlap one kernel's tail
+        with the next's ramp)."""
         launches = 0
         for i, (name, r, c, G, x, codes, scales) in enumerate(bufs):
-            s = streams[i % len(streams)] if streams else torch.cuda.current_stream()
+            s = streams[branch_of(i)] if streams else torch.cuda.current_stream()
             am = amax.data_ptr() + 4 * i
             if record is not None:
                 record[name][0].record(s)
@@ -823,6 +911,12 @@ def run_mgaq(args, extra_mode=False):
         torch.cuda.synchronize()
     ms = start.elapsed_time(end) / reps
     launches = launches_per_step * reps
+    # one more step inside an NVTX range: the unit `ncu --nvtx --nvtx-include
+    # cfg2_layer/ --graph-profiling graph` measures (profiles/mgaq_dram_bytes.json)
+    torch.cuda.nvtx.range_push("cfg2_layer")
+    run_once()
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
     # per-tensor timing from one extra instrumented (eager) pass
     step(evs)
     torch.cuda.synchronize()

@@ -18,6 +18,7 @@
 // occur where the E4M3 code is +-0 or saturated either way -- then one
 // cvt.e4m3x2 encodes two elements.  Codes are bit-identical to the reference.
 #include <cstdint>
+#include <cstdlib>
 
 #include "coat_device.cuh"
 #include "coat_internal.h"
@@ -138,17 +139,35 @@ dequant_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ s
 // ------------------------------------------------- Group Scaling amax (K3) ----
 // Stage 1: per-1xG absmax -> intermediate (optional).  Stage 2: global max via
 // a block max + one atomicMax per CTA on the fp32 bit pattern.
+//
+// The per-tensor encode that follows reads x again; the amax pass marks the
+// LAST kL2KeepBytes of x L2::evict_last (the rest evict_first) and the encode
+// pass walks the chunks in reverse, so the resident tail is consumed first: a
+// tensor up to the budget is read from DRAM once, a larger one (down.in,
+// 180 MB > the 126 MB L2) re-reads only its head instead of all of it.
+// COAT_L2_KEEP_MB overrides the budget (A/B measurements).
+int64_t l2_keep_chunks(int64_t nchunks, int esz) {
+    static const int64_t keep_bytes = [] {
+        const char* e = getenv("COAT_L2_KEEP_MB");
+        return (e && *e ? int64_t(atoi(e)) : int64_t(80)) << 20;
+    }();
+    const int64_t keep = keep_bytes / (16 * esz);
+    return nchunks > keep ? nchunks - keep : 0;   // first chunk kept resident
+}
+
 template <int DT, int L>
 __global__ void __launch_bounds__(kThreads)
 group_amax_kernel(const void* __restrict__ x, int64_t nchunks, float* __restrict__ inter,
-                  uint32_t* global_bits) {
+                  uint32_t* global_bits, int64_t keep_from) {
     __shared__ uint32_t wmax[kThreads / 32];
     uint32_t gm = 0;
     for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch - threadIdx.x % 32 < nchunks;
          ch += int64_t(gridDim.x) * kThreads) {
         const bool valid = ch < nchunks;
         uint32_t am = 0;
-        if (valid) am = absmax_raw<DT, true>(load_raw16<DT, EV_LAST>(x, ch * 16));
+        if (valid)
+            am = absmax_raw<DT, true>(ch >= keep_from ? load_raw16<DT, EV_LAST>(x, ch * 16)
+                                                      : load_raw16<DT, EV_FIRST>(x, ch * 16));
 #pragma unroll
         for (int off = 1; off < L; off <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, off));
         if (valid && inter && (threadIdx.x % L) == 0) inter[ch / L] = u2f(am);
@@ -191,9 +210,11 @@ quant_tensor_kernel(const void* __restrict__ x, int64_t n, const uint32_t* amax_
     if (blockIdx.x == 0 && threadIdx.x == 0 && scale_out) *scale_out = float_to_bf16_bits_exact(s);
     uint32_t bad = 0;
     const int64_t nchunks = n / 16;
-    for (int64_t ch = blockIdx.x * int64_t(kThreads) + threadIdx.x; ch < nchunks;
-         ch += int64_t(gridDim.x) * kThreads) {
-        // second (last) pass over x: the amax pass left it in L2 (evict_last)
+    for (int64_t it = blockIdx.x * int64_t(kThreads) + threadIdx.x; it < nchunks;
+         it += int64_t(gridDim.x) * kThreads) {
+        // second (last) pass over x, tail first: the amax pass left the tail in
+        // L2 (evict_last, l2_keep_chunks)
+        const int64_t ch = nchunks - 1 - it;
         const RawChunk<DT> raw = A32 ? load_raw16<DT, EV_FIRST>(x, ch * 16) : load_raw16_a16<DT>(x, ch * 16);
         bad |= absmax_raw<DT, false>(raw) >= 0x7F800000u;
         reinterpret_cast<uint4*>(codes)[ch] = encode16(widen16<DT>(raw), s, inv_s, nz);
@@ -305,9 +326,11 @@ cudaError_t launch_group_amax(const void* x, int dtype, int64_t n, int64_t G, fl
     if (pow2_lanes(G, &L) && aligned32(x)) {
         const int64_t nchunks = n / 16;
         if (dtype == 0) {
-            COAT_GROUP_SWITCH(L, (group_amax_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, inter, global_bits)));
+            const int64_t kf = l2_keep_chunks(nchunks, 4);
+            COAT_GROUP_SWITCH(L, (group_amax_kernel<0, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, inter, global_bits, kf)));
         } else {
-            COAT_GROUP_SWITCH(L, (group_amax_kernel<1, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, inter, global_bits)));
+            const int64_t kf = l2_keep_chunks(nchunks, 2);
+            COAT_GROUP_SWITCH(L, (group_amax_kernel<1, L><<<blocks_for(nchunks), kThreads, 0, st>>>(x, nchunks, inter, global_bits, kf)));
         }
     } else {
         const int blocks = blocks_for((n / G) * 32);

@@ -288,6 +288,10 @@ cudaError_t launch_mgaq_streams(const MgaqItem* items, int n, uint32_t* flags, c
     if ((e = cudaEventRecord(ss.fork, st)) != cudaSuccess) return e;
     for (int k = 0; k < kBatchStreams; ++k)
         if ((e = cudaStreamWaitEvent(ss.s[k], ss.fork, 0)) != cudaSuccess) return e;
+    // Items round-robin over the streams.  (Measured round 2: all per-tensor
+    // items on one stream -- one L2-resident tensor at a time -- cuts the
+    // layer's DRAM traffic from 1.17x to 1.12x the algorithmic bytes but
+    // serialises 8 short kernels: 0.330 vs 0.318 ms.)
     for (int i = 0; i < n; ++i) {
         const MgaqItem& m = items[i];
         cudaStream_t sk = ss.s[i % kBatchStreams];

@@ -201,3 +201,91 @@ class ZeroAdamW:
         finally:
             if weights_change:
                 all_gather_params(w_full, self.slot._w_scratch, self.group)
+
+
+class PeerZeroAdamW:
+    """ZeroAdamW with the two collectives as SM kernels over NVLink peer memory
+    (coat_zero_step_p2p) instead of NCCL: the gradient and
+    both weight buffers live in torch symmetric memory, so every rank maps
+    every other rank's copy.  Per step the reduce-scatter reads the peers'
+    gradient shards in place (P2P loads summed in rank order, or NVLink-SHARP
+    multimem.ld_reduce when the platform gives a multicast address and the
+    wire is fp32), K1 steps the shard, and the new shard is stored straight
+    into every rank's next-weight buffer (P2P or multimem.st) -- chunk by
+    chunk, so the NVLink traffic overlaps the step.  The weights are
+    double-buffered: ``weights`` is the current buffer, the step writes the
+    other one and the commit flips them -- unless the OR of the ranks' error
+    words says the reference's step would have thrown before touching the
+    parameters (optimizer.cpp:101-114).
+
+    Usage: write this rank's gradients into ``grad`` (fp32, or bf16 with
+    ``grad_dtype=torch.bfloat16`` for the half-width wire), call ``step()``,
+    read the parameters from ``weights``."""
+
+    def __init__(self, shapes: Sequence[Sequence[int]], cfg: coatsim.AdamWConfig | None = None, group=None,
+                 device=None, grad_dtype: torch.dtype = torch.float32, multicast: bool = True, chunk: int = 0):
+        import ctypes as C
+
+        import torch.distributed._symmetric_memory as symm_mem
+        if grad_dtype not in (torch.float32, torch.bfloat16):
+            raise coatsim.InvalidSpec("PeerZeroAdamW: gradients are float32 or bfloat16")
+        self.group = group if group is not None else dist.group.WORLD
+        self.world_size, self.rank = _world(self.group)
+        self.layout = FlatLayout.build(shapes, self.world_size)
+        self.lo, self.hi = self.layout.shard(self.rank)
+        self.cfg = cfg or coatsim.AdamWConfig()
+        self.chunk = int(chunk)
+        device = torch.device(device or "cuda", torch.cuda.current_device()) if not isinstance(device, torch.device) \
+            else device
+        n = self.layout.total
+        self.grad = symm_mem.empty(n, dtype=grad_dtype, device=device)
+        self._w = [symm_mem.empty(n, dtype=torch.float32, device=device) for _ in range(2)]
+        self._w[0].zero_()
+        name = self.group.group_name
+        self._hg = symm_mem.rendezvous(self.grad, name)
+        hw = [symm_mem.rendezvous(w, name) for w in self._w]
+        P = C.c_void_p * self.world_size
+        self._g_peers = P(*self._hg.buffer_ptrs)
+        self._w_peers = [P(*h.buffer_ptrs) for h in hw]
+        use_mc = multicast and grad_dtype == torch.float32
+        self._g_mc = (self._hg.multicast_ptr or None) if use_mc else None
+        self._w_mc = [(h.multicast_ptr or None) if multicast else None for h in hw]
+        self._g_dtype = 0 if grad_dtype == torch.float32 else 1
+        self._cur = 0
+        self.slot = coatsim.make_slot([self.hi - self.lo], device=device)
+        self.g_shard = torch.empty(self.hi - self.lo, dtype=torch.float32, device=device)
+
+    @property
+    def weights(self) -> torch.Tensor:
+        return self._w[self._cur]
+
+    @property
+    def uses_multicast(self) -> bool:
+        return self._g_mc is not None
+
+    @property
+    def step_count(self) -> int:
+        return self.slot.step
+
+    def step(self) -> None:
+        import ctypes as C
+        L = _lib.lib
+        slot, nxt = self.slot, 1 - self._cur
+        # every rank's gradients (and the previous step's weight stores) are
+        # complete before any rank reads them
+        self._hg.barrier()
+        mi, vi = slot._m[slot._cm], slot._v[slot._cv]
+        mo, vo = slot._m[1 - slot._cm], slot._v[1 - slot._cv]
+        slot._flags.t.zero_()
+        c = self.cfg.c_struct()
+        coatsim._check(L.coat_zero_step_p2p(
+            self._g_peers, self._g_mc, self._g_dtype, self._w_peers[nxt], self._w_mc[nxt],
+            self._w[self._cur].data_ptr(), self._w[nxt].data_ptr(), self.layout.total, GROUP, mi.c_struct(),
+            vi.c_struct(), mo.c_struct(), vo.c_struct(), C.byref(c), slot.step + 1, self.g_shard.data_ptr(),
+            slot._flags.ptr, self.rank, self.world_size, self.chunk, coatsim._stream()))
+        # the OR of the error words; also the point after which every rank's
+        # stores into this rank's next-weight buffer have landed
+        flags = _all_flags(slot._flags.t, self.group)
+        if not (flags & (_lib.FLAG_NONFINITE_GRAD | _lib.FLAG_CONTRACT)):
+            self._cur = nxt
+        coatsim._step_commit(None, slot, flags)

@@ -155,3 +155,79 @@ def test_p2p_step_validates_before_any_work():
                                 16, 16, 0, 17, 0, None) == 5
     assert L.coat_zero_step_p2p(None, 16, 1, one, None, 16, 16, 1024, 128, ms, ms, ms, ms, C.byref(cfg), 1, 16,
                                 16, 0, 1, 0, None) == 5
+
+
+SHAPES = [(300,), (5, 128), (1000,), (64, 96), (7000,)]
+
+
+def _peer_worker(port, grad_dtype, q):
+    import os
+    import sys
+    from conftest import ROOT
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2410_19313_b200 import coatsim
+        from paper_2410_19313_b200.zero import PeerZeroAdamW
+        dt = torch.bfloat16 if grad_dtype == "bf16" else torch.float32
+        z = PeerZeroAdamW(SHAPES, coatsim.AdamWConfig(**CFG), grad_dtype=dt, chunk=2048 * 3)
+        lay = z.layout
+        r = np.random.default_rng(5)
+        ws0 = [(r.standard_normal(int(np.prod(s))) * 0.02).astype(np.float32) for s in SHAPES]
+        z.weights.copy_(lay.flatten([torch.from_numpy(w).reshape(s).cuda() for w, s in zip(ws0, SHAPES)]))
+        grads = []
+        for t in range(3):
+            gs = [(r.standard_normal(int(np.prod(s))) * 1e-3).astype(np.float32) for s in SHAPES]
+            gflat = lay.flatten([torch.from_numpy(g).reshape(s).cuda() for g, s in zip(gs, SHAPES)])
+            z.grad.copy_(gflat.to(dt))
+            grads.append([x.cpu().numpy() for x in lay.views(z.grad.float())])
+            z.step()
+        torch.cuda.synchronize()
+        w = [x.cpu().numpy().copy() for x in lay.views(z.weights)]
+        z.grad[lay.offsets[2] + 5] = float("nan")
+        before = z.weights.clone()
+        raised = None
+        try:
+            z.step()
+        except coatsim.Error as e:
+            raised = type(e).__name__
+        q.put(("ok", {"w0": ws0, "grads": grads, "w": w, "raised": raised, "same": bool(torch.equal(z.weights, before)),
+                      "steps": z.step_count, "mc": z.uses_multicast}))
+    except Exception:
+        import traceback
+        q.put(("err", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grad_dtype", ["fp32", "bf16"])
+def test_peer_zero_adamw_symmetric_memory(checker, grad_dtype):
+    """zero.PeerZeroAdamW end to end on torch symmetric memory (one rank: the
+    one GPU), per-tensor parity against the checker, and the reference's
+    NonFiniteGradient commit semantics on the double-buffered weights."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_peer_worker, args=(port, grad_dtype, q))
+    p.start()
+    status, res = q.get(timeout=600)
+    p.join(timeout=120)
+    assert status == "ok", res
+    for i, s in enumerate(SHAPES):
+        n = int(np.prod(s))
+        w = res["w0"][i].copy()
+        m, v = checker.make_slot(n)
+        for t in range(3):
+            assert checker.step(w, res["grads"][t][i].reshape(-1), m, v, t, CFG) == 0
+        assert np.array_equal(res["w"][i].reshape(-1).view(np.uint32), w.view(np.uint32)), (grad_dtype, i)
+    assert res["raised"] == "NonFiniteGradient" and res["same"] and res["steps"] == 3, res
