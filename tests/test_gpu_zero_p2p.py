@@ -231,3 +231,98 @@ def test_peer_zero_adamw_symmetric_memory(checker, grad_dtype):
             assert checker.step(w, res["grads"][t][i].reshape(-1), m, v, t, CFG) == 0
         assert np.array_equal(res["w"][i].reshape(-1).view(np.uint32), w.view(np.uint32)), (grad_dtype, i)
     assert res["raised"] == "NonFiniteGradient" and res["same"] and res["steps"] == 3, res
+
+
+def _ipc_worker(rank, ws, q_out, q_peers, barrier):
+    import ctypes as C
+    import sys
+    from conftest import ROOT
+    sys.path.insert(0, ROOT)
+    import torch
+    torch.cuda.set_device(0)
+    try:
+        from paper_2410_19313_b200 import _lib
+        L = _lib.lib
+        n = 128 * 1500 + 128 * 3
+        N = n * ws
+        r = np.random.default_rng(77)
+        w0 = (r.standard_normal(N) * 0.02).astype(np.float32)
+        g = torch.empty(N, device="cuda")
+        w = [torch.from_numpy(w0).cuda(), torch.full((N,), float("nan"), device="cuda")]
+        # every process maps every other process's gradient and weight buffers (CUDA IPC)
+        for k in range(ws):
+            if k != rank:
+                q_peers[k].put((rank, g, w[0], w[1]))
+        peers = {rank: (g, w[0], w[1])}
+        while len(peers) < ws:
+            rk, a, b, c = q_peers[rank].get(timeout=300)
+            peers[rk] = (a, b, c)
+        barrier.wait()
+        gp = (C.c_void_p * ws)(*[peers[k][0].data_ptr() for k in range(ws)])
+        wp = [(C.c_void_p * ws)(*[peers[k][1 + j].data_ptr() for k in range(ws)]) for j in range(2)]
+        m, v = [_moment(n, torch), _moment(n, torch)], [_moment(n, torch), _moment(n, torch)]
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        g_shard = torch.empty(n, device="cuda")
+        cfg = _lib.AdamWConfigC(**CFG)
+        st = torch.cuda.current_stream().cuda_stream
+        grads = []
+        cur = 0
+        for t in range(1, 4):
+            gh = (np.random.default_rng(1000 * t + rank).standard_normal(N) * 1e-3).astype(np.float32)
+            grads.append(gh)
+            g.copy_(torch.from_numpy(gh))
+            torch.cuda.synchronize()
+            barrier.wait()                      # every rank's gradients are in place
+            a, b = (t - 1) % 2, t % 2
+            assert L.coat_zero_step_p2p(gp, None, 0, wp[1 - cur], None, w[cur].data_ptr(), w[1 - cur].data_ptr(),
+                                        N, 128, _cs(_lib, m[a]), _cs(_lib, v[a]), _cs(_lib, m[b]), _cs(_lib, v[b]),
+                                        C.byref(cfg), t, g_shard.data_ptr(), flags.data_ptr(), rank, ws, 2048 * 7,
+                                        st) == 0, L.coat_last_error()
+            torch.cuda.synchronize()
+            assert int(flags.item()) == 0
+            barrier.wait()                      # every rank's stores into every next-weight buffer landed
+            cur = 1 - cur
+        st_out = {k: m[1][k].cpu().numpy().copy() for k in ("codes", "k", "c")}
+        st_out["scales"] = m[1]["scales"].cpu().numpy().copy()
+        q_out.put((rank, "ok", {"w": w[cur].cpu().numpy().copy(), "grads": grads, "w0": w0, "m": st_out, "n": n}))
+        barrier.wait()                          # peers keep their buffers alive until everyone is done
+    except Exception:
+        import traceback
+        q_out.put((rank, "err", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_p2p_step_separate_processes_ipc(checker, ws):
+    """coat_zero_step_p2p across real process boundaries: every rank is its own
+    process on the one GPU and maps the other ranks' gradient and weight
+    buffers through CUDA IPC (torch.multiprocessing), as ranks on an NVLink
+    node map each other's memory.  Final weights on every rank and rank 0's
+    first-moment shard against the checker's step on the rank-order sum."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q_out, barrier = ctx.Queue(), ctx.Barrier(ws)
+    q_peers = [ctx.Queue() for _ in range(ws)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, ws, q_out, q_peers, barrier)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(ws):
+        rk, status, d = q_out.get(timeout=600)
+        assert status == "ok", f"rank {rk}: {d}"
+        res[rk] = d
+    for p in procs:
+        p.join(timeout=120)
+    n = res[0]["n"]
+    N = n * ws
+    w_ref = res[0]["w0"].copy()
+    m, v = checker.make_slot(N)
+    for t in range(3):
+        gsum = res[0]["grads"][t].copy()
+        for rk in range(1, ws):
+            gsum = (gsum + res[rk]["grads"][t]).astype(np.float32)
+        assert checker.step(w_ref, gsum, m, v, t, CFG) == 0
+    for rk in range(ws):
+        assert np.array_equal(res[rk]["w"].view(np.uint32), w_ref.view(np.uint32)), rk
+    mine = res[0]["m"]
+    assert np.array_equal(mine["codes"], m["codes"][:n])
+    assert np.array_equal(mine["k"], m["k"][:n // 128]) and np.array_equal(mine["c"], m["c"][:n // 128])
