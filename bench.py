@@ -1061,26 +1061,45 @@ def run_mgaq_fused(args, extra_mode=False):
 
 
 # ----------------------------------------------- cfg4: FP8 linear fwd+bwd ----
-def fp8_burst_peak_tflops():
-    """cuBLASLt FP8 (E4M3 x E4M3 -> bf16, torch._scaled_mm) at 8192^3, best of 10
-    back-to-back timings -- the measured FP8 denominator of cfg4's roofline."""
+def fp8_peak_tflops():
+    """cuBLASLt FP8 (E4M3 x E4M3 -> bf16, torch._scaled_mm) at 8192^3: the burst
+    figure (best of 10 short timings) and the sustained one (back to back for
+    3 s, the way MEASURED_PEAKS.json's bf16_tflops_sustained is taken) -- the
+    measured FP8 denominators of cfg4's roofline.  K4's forward is timed inside
+    a >= 1 s loop of the whole cfg4 step, so the sustained figure is the one
+    its frac uses (the B200 drops its clocks under the power cap within
+    ~100 ms of tensor-core load)."""
     import torch
     n = 8192
     a = torch.randn(n, n, device="cuda").to(torch.float8_e4m3fn)
     b = torch.randn(n, n, device="cuda").to(torch.float8_e4m3fn).t()
     one = torch.ones((), device="cuda")
+    mm = lambda: torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
     for _ in range(3):
-        torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        mm()
     best = 1e9
     for _ in range(10):
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
         for _ in range(5):
-            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+            mm()
         s1.record()
         torch.cuda.synchronize()
         best = min(best, s0.elapsed_time(s1) / 5)
-    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    flop = 2.0 * n ** 3
+    reps = 0
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    s0.record()
+    while time.perf_counter() - t0 < 3.0:
+        for _ in range(20):
+            mm()
+        reps += 20
+        torch.cuda.synchronize()
+    s1.record()
+    torch.cuda.synchronize()
+    sustained = flop * reps / (s0.elapsed_time(s1) * 1e-3) / 1e12
+    return flop / (best * 1e-3) / 1e12, sustained
 
 
 def linear_cpu_baseline(rows=16):
@@ -1177,12 +1196,18 @@ def run_linear(args, extra_mode=False):
     ms = sum(per.values())
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            bf16_peak = float(json.load(f)["bf16_tflops"])
-        bf16_kind = "measured bf16 (MEASURED_PEAKS.json, cuBLAS burst)"
+            mp = json.load(f)
+        bf16_peak = float(mp.get("bf16_tflops_sustained") or mp["bf16_tflops"])
+        bf16_kind = ("measured bf16 (MEASURED_PEAKS.json, cuBLAS sustained: dgrad / wgrad are timed inside the "
+                     ">= 1 s cfg4 loop)" if mp.get("bf16_tflops_sustained") else
+                     "measured bf16 (MEASURED_PEAKS.json, cuBLAS burst)")
     except Exception:
         bf16_peak, bf16_kind = 1590.0, "fallback"
+    fp8_burst = None
     try:
-        fp8_peak, kind = fp8_burst_peak_tflops(), "measured here: cuBLASLt FP8 _scaled_mm 8192^3 burst"
+        fp8_burst, fp8_peak = fp8_peak_tflops()
+        kind = ("measured here: cuBLASLt FP8 _scaled_mm 8192^3 back to back for 3 s (sustained; the forward "
+                "is timed inside a >= 1 s loop of the cfg4 step)")
     except Exception as ex:
         fp8_peak, kind = 2 * bf16_peak, f"2x bf16 (FP8 probe failed: {ex!r:.80})"
     cpu = None if args.no_cpu_baseline else linear_cpu_baseline()
@@ -1198,6 +1223,8 @@ def run_linear(args, extra_mode=False):
         "per_phase_ms": per, "tflops": tf,
         "roofline": {"bound": "tensor", "achieved": tf["fwd"], "peak": fp8_peak, "unit": "TFLOP/s",
                      "frac": tf["fwd"] / fp8_peak, "traffic": None, "peak_kind": kind,
+                     "fp8_burst_peak": fp8_burst,
+                     "frac_of_burst": tf["fwd"] / fp8_burst if fp8_burst else None,
                      "frac_of_nominal_4500": tf["fwd"] / 4500.0, "kernel": "gemm_kernel (K4) FP8 forward",
                      "bwd_frac_of_bf16": {"dgrad": tf["dgrad"] / bf16_peak, "wgrad": tf["wgrad"] / bf16_peak},
                      "bf16_peak": bf16_peak, "bf16_peak_kind": bf16_kind},
