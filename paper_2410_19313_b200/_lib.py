@@ -71,6 +71,7 @@ _SIGS = {
     "coat_test_pack_prepare": ([_vp, _vp, _i64, C.c_double, _vp, _vp], _int),
     "coat_test_expf_neg2": ([C.c_uint64, C.c_uint64, _vp, _vp], _int),
     "coat_test_k1_layout": ([], _int),
+    "coat_test_cta_tables": ([_vp, _vp], _int),
     "coat_test_mufu_bounds": ([C.c_float, C.c_float, C.c_float, _vp, _vp], _int),
     "coat_flags_to_status": ([C.c_uint32], _int),
     "coat_device_sm_count": ([], _int),

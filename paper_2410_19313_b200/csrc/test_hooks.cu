@@ -117,4 +117,23 @@ extern "C" int coat_test_expf_neg2(uint64_t first, uint64_t count, unsigned long
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+namespace coat {
+namespace {
+__global__ void cta_tables_dump_kernel(double* out) {
+    __shared__ dre::CtaTables T;
+    dre::init_cta_tables(T, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const double* src = reinterpret_cast<const double*>(&T);
+    for (int i = threadIdx.x; i < int(sizeof(dre::CtaTables) / sizeof(double)); i += blockDim.x) out[i] = src[i];
+}
+}  // namespace
+}  // namespace coat
+
+// coat_test_cta_tables: the CTA constant tables (dre::CtaTables) as the device
+// computes them (generator and check of csrc/cta_tables_data.h).
+extern "C" int coat_test_cta_tables(double* out, void* stream) {
+    coat::cta_tables_dump_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 extern "C" int coat_test_k1_layout() { return coat::k1_ws_config(); }

@@ -119,3 +119,4 @@ def test_mufu_error_bounds():
     print(f"lg2.approx max err / (1 + |log2 r|) 2^{math.log2(e_lg):.2f}, ex2.approx max rel err "
           f"2^{math.log2(e_ex):.2f}")
     assert e_lg <= 2.0 ** -22 and e_ex <= 2.0 ** -22
+
