@@ -50,3 +50,30 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "pyoracle" not in text and "coat_oracle" not in text and "oracle/" not in text, f
+
+
+def test_round2_entry_points_validate_without_gpu():
+    """The peer-memory ZeRO step and the quantizing GEMM epilogues reject bad
+    geometry / arguments synchronously, before any device work (the reference
+    throws before mutating anything)."""
+    from paper_2410_19313_b200 import _lib
+    L = _lib.lib
+    cfg = _lib.AdamWConfigC(beta1=0.9, beta2=0.999, lr=1e-3, weight_decay=0.1, eps=1e-8)
+    ms = _lib.MomentState(None, None, None, None)
+    one = (ctypes.c_void_p * 1)(16)
+    # coat_zero_step_p2p: n_total % (128 * nranks) -> GEOMETRY; bad rank / 17 ranks / bf16 multimem -> INVALID
+    assert L.coat_zero_step_p2p(one, None, 0, one, None, 16, 16, 1000, 128, ms, ms, ms, ms, ctypes.byref(cfg), 1,
+                                16, 16, 0, 1, 0, None) == 2
+    assert L.coat_zero_step_p2p(one, None, 0, one, None, 16, 16, 1024, 128, ms, ms, ms, ms, ctypes.byref(cfg), 1,
+                                16, 16, 1, 1, 0, None) == 5
+    assert L.coat_zero_step_p2p(None, 16, 1, one, None, 16, 16, 1024, 128, ms, ms, ms, ms, ctypes.byref(cfg), 1,
+                                16, 16, 0, 1, 0, None) == 5
+    # misaligned peer pointer -> INVALID
+    odd = (ctypes.c_void_p * 1)(8)
+    assert L.coat_zero_step_p2p(odd, None, 0, one, None, 16, 16, 1024, 128, ms, ms, ms, ms, ctypes.byref(cfg), 1,
+                                16, 16, 0, 1, 0, None) == 5
+    # quantizing epilogues: K or N not a multiple of 16 -> SHAPE; NULL scales -> INVALID
+    assert L.coat_fp8_linear_fwd_q16(16, None, 16, None, 128, 100, 128, 16, 16, None, None, None) == 1
+    assert L.coat_fp8_linear_fwd_q16(16, None, 16, None, 128, 128, 128, 16, None, None, None, None) == 5
+    assert L.coat_fp8_upgate_silu_quant(16, None, 16, None, 16, None, 128, 128, 200, *([16] * 8), None, None, None,
+                                        16, None, None) == 1
