@@ -521,7 +521,8 @@ def run_zero_p2p(args, L, _lib, P, n, ws, rank, m, v, cur, t_step, cfg, flags, g
     import torch.distributed._symmetric_memory as symm_mem
     free, _ = torch.cuda.mem_get_info()
     need = 3 * 4 * P
-    fits = torch.tensor([1 if need <= free * 0.95 else 0], dtype=torch.int32, device=dev)
+    fits = torch.tensor([1 if need <= free * 0.95 else 0], dtype=torch.int32,
+                        device="cpu" if dist.get_backend() == "gloo" else dev)
     dist.all_reduce(fits, op=dist.ReduceOp.MIN)    # every rank takes the same decision (rendezvous is collective)
     if not int(fits.item()):
         return {"unavailable": f"needs {need / 1e9:.1f} GB of symmetric memory per rank, {free / 1e9:.1f} GB free"}
