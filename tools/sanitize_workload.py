@@ -8,6 +8,10 @@ family, for `compute-sanitizer --tool racecheck|synccheck|memcheck`
          (COAT_MGAQ_BATCH selects the internal-stream or cooperative form)
   gemm   the FP8 forward and the BF16 dgrad / wgrad (COAT_GEMM_CTA=1: the
          single-CTA kernel; default the CTA-pair kernel)
+  epi    the quantizing GEMM epilogues: per-group 1x16 output and the fused
+         gate/up + SiLU*mul block (+ its down.in pass)
+  p2p    coat_zero_step_p2p on 2 virtual ranks (peer-load reduce-scatter, K1,
+         peer-store all-gather, chunk-pipelined over three streams)
 Results are checked loosely (finite, right shapes) -- the parity suites do the
 bit-exact checks; this exercises the synchronisation under the sanitizer.
 """
@@ -53,6 +57,39 @@ def main(which):
         dw = coat.linear_wgrad(qx, dy)
         torch.cuda.synchronize()
         assert torch.isfinite(y).all() and torch.isfinite(dx.float()).all() and torch.isfinite(dw).all()
+    elif which == "epi":
+        M, K, N = 256, 512, 400
+        x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        qx = coat.quantize(x, coat.QuantGeometry.per_tensor())
+        qg = coat.quantize(torch.randn(K, N, device="cuda") / K ** 0.5, coat.QuantGeometry.per_tensor())
+        qu = coat.quantize(torch.randn(K, N, device="cuda") / K ** 0.5, coat.QuantGeometry.per_tensor())
+        q16 = coat.fp8_linear_q16(qx, qg)
+        recs = coat.fp8_upgate_silu(qx, qg, qu)
+        torch.cuda.synchronize()
+        assert q16.codes.shape == (M, N) and len(recs) == 4
+    elif which == "p2p":
+        import ctypes as C
+        from paper_2410_19313_b200 import _lib
+        L = _lib.lib
+        nranks, n = 2, 2048 * 3 + 128 * 5
+        N = n * nranks
+        cfg = _lib.AdamWConfigC(beta1=0.9, beta2=0.999, lr=1e-3, weight_decay=0.1, eps=1e-8)
+        g = [torch.randn(N, device="cuda") * 1e-3 for _ in range(nranks)]
+        w = [torch.randn(N, device="cuda") * 0.02 for _ in range(nranks)]
+        wn = [torch.empty(N, device="cuda") for _ in range(nranks)]
+        ptrs = lambda ts: (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+        st = torch.cuda.current_stream().cuda_stream
+        for r in range(nranks):
+            sl = [coat.make_slot([n]) for _ in range(2)]
+            flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+            gs = torch.empty(n, device="cuda")
+            m0, v0 = sl[0]._m[0].c_struct(), sl[0]._v[0].c_struct()
+            m1, v1 = sl[0]._m[1].c_struct(), sl[0]._v[1].c_struct()
+            assert L.coat_zero_step_p2p(ptrs(g), None, 0, ptrs(wn), None, w[r].data_ptr(), wn[r].data_ptr(), N, 128,
+                                        m0, v0, m1, v1, C.byref(cfg), 1, gs.data_ptr(), flags.data_ptr(), r, nranks,
+                                        2048 * 2, st) == 0, L.coat_last_error()
+        torch.cuda.synchronize()
+        assert all(torch.isfinite(x).all() for x in wn)
     else:
         raise SystemExit(f"unknown workload {which}")
     print(f"sanitize workload {which} ok")
