@@ -46,6 +46,17 @@ constexpr int BN = 256;                   // accumulator columns (MMA N)
 constexpr int BKB = 128;                  // K bytes per stage (one 128B swizzle row)
 constexpr int A_BYTES = BM * BKB;         // 16 KiB
 constexpr int THREADS = 192;
+// Epilogue warps: 4 (one per TMEM lane quarter) -- or 8 for the quantizing
+// gate/up epilogue, whose per-element work (three quantizers + SiLU) is longer
+// than the MMA main loop of a tile with 4 warps (ncu: tensor pipe 62%); the
+// second four take the other half of the accumulator's columns.
+#ifndef COAT_GEMM_EPI8_ALL
+#define COAT_GEMM_EPI8_ALL 0
+#endif
+template <int kOut>
+__host__ __device__ constexpr int epi_warps() { return (kOut == 3 || COAT_GEMM_EPI8_ALL) ? 8 : 4; }
+template <int kOut>
+__host__ __device__ constexpr int threads_for() { return 64 + 32 * epi_warps<kOut>(); }
 constexpr int ACC_COLS = BN;              // fp32 columns per accumulator
 constexpr int TMEM_COLS = 2 * ACC_COLS;   // double buffer = all 512 columns
 
@@ -233,7 +244,7 @@ __device__ __forceinline__ uint32_t quant16_store(const aq::Chunk16& y, uint8_t*
 }
 
 template <bool kF8, bool kAMN, bool kBMN, int kOut, int kCta>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(threads_for<kOut>(), 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             const __grid_constant__ CUtensorMap map_b2, Params P) {
     static_assert(kOut != kOutUpGate || (kF8 && kBMN), "gate/up epilogue: FP8 forward, W (K, N) row-major");
@@ -263,7 +274,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4 * kCta);   // one arrive per epilogue warp of the pair
+            mbar_init(&tempty[a], epi_warps<kOut>() * kCta);   // one arrive per epilogue warp of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -399,8 +410,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             }
         }
     } else {
-        // ------------------------------------------------------ epilogue (warps 2..5)
+        // ------------------------------------------------------ epilogue (warps 2 .. 1 + epi_warps)
         const int q = warp & 3;                    // TMEM lane quarter this warp may access
+        const int half = epi_warps<kOut>() == 8 ? (warp - 2) >> 2 : 0;   // 8 warps: which column half
         const int row_in_tile = int(rank) * BM + q * 32 + lane;
         const uint32_t tempty_leader0 = kCta == 2 ? cluster_addr(&tempty[0], 0) : 0u;
         float alpha = P.alpha;
@@ -423,7 +435,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 const bool live = row < P.M;
                 const int64_t rq = live ? row : 0;
 #pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
+                constexpr int kChunks = 16 / epi_warps<kOut>();   // 32-column chunks per warp (of 4)
+                for (int c = half * kChunks; c < (half + 1) * kChunks; ++c) {
                     uint32_t rg[32], ru[32];
                     tmem_ld32(taddr + uint32_t(c * 32), rg);
                     tmem_ld32(taddr + uint32_t(128 + c * 32), ru);
@@ -468,7 +481,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 }
             } else
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half * (BN / 32) * 4 / epi_warps<kOut>(); c < (half + 1) * (BN / 32) * 4 / epi_warps<kOut>();
+                 ++c) {
                 uint32_t r[32];
                 tmem_ld32(taddr + uint32_t(c * 32), r);
                 tmem_wait_ld();
@@ -628,12 +642,12 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     const int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
     const int grid = kCta * (ntiles < units ? ntiles : units);
     if (kCta == 1) {
-        kern<<<grid, THREADS, G::SMEM_BYTES, stream>>>(ma, mb, mb2, P);
+        kern<<<grid, threads_for<kOut>(), G::SMEM_BYTES, stream>>>(ma, mb, mb2, P);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(threads_for<kOut>());
     cfg.dynamicSmemBytes = G::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
