@@ -811,12 +811,20 @@ def run_mgaq(args, extra_mode=False):
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     nel = sum(r * c for _, r, c, *_ in bufs)
 
+    plan = os.environ.get("COAT_BENCH_MGAQ_PLAN", "rr")
+
     def branch_of(i):
         """Records round-robin over the branches (as coat_quantize_batch's
         streams).  Measured round 2: the per-tensor records all on one branch
         (one L2-resident tensor at a time) cut the DRAM traffic from 1.17x to
         1.12x the algorithmic bytes but serialise 8 short kernels: 0.330 vs
-        0.318 ms."""
+        0.318 ms.  COAT_BENCH_MGAQ_PLAN=ptK (measurement): per-tensor records
+        round-robin over the first K branches, per-group over the others."""
+        if plan.startswith("pt") and nbr > int(plan[2:]):
+            k = int(plan[2:])
+            G = bufs[i][3]
+            j = sum(1 for q in range(i) if bool(bufs[q][3]) == bool(G))
+            return j % k if not G else k + j % (nbr - k)
         return i % nbr
 
     nbr = max(1, args.mgaq_branches)

@@ -463,9 +463,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                         const int64_t co = rq * P.q.ldc + col, so = rq * (P.q.ldc >> 4) + (col >> 4);
                         uint4 cw;
                         uint16_t sbits;
-                        bad |= aq::quant_dq16(gv, cw, sbits, -0.0f);   // silu.in
+                        float gam;
+                        bad |= aq::quant_dq16(gv, cw, sbits, -0.0f, &gam);   // silu.in
                         if (live) { *reinterpret_cast<uint4*>(P.q.c0 + co) = cw; P.q.s0[so] = sbits; }
-                        aq::silu16(gv, -0.0f);
+                        aq::silu16(gv, -0.0f, gam);
                         bad |= aq::quant_dq16(gv, cw, sbits, -0.0f);   // mul.in.silu
                         if (live) { *reinterpret_cast<uint4*>(P.q.c1 + co) = cw; P.q.s1[so] = sbits; }
                         bad |= aq::quant_dq16(uv, cw, sbits, -0.0f);   // mul.in.up
