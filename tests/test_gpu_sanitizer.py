@@ -24,23 +24,46 @@ CASES = [("k1", {"COAT_K1_EW": "8"}), ("k1", {"COAT_K1_EW": "7"}), ("k1", {"COAT
          ("p2p", {})]
 
 
-@pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
-@pytest.mark.parametrize("which,env", CASES, ids=[f"{w}-{'-'.join(f'{k}={v}' for k, v in e.items()) or 'default'}"
-                                                  for w, e in CASES])
-def test_compute_sanitizer_clean(tool, which, env):
-    if not os.path.exists(SANITIZER):
-        pytest.skip("compute-sanitizer not installed")
+TOOLS = ["racecheck", "synccheck", "memcheck"]
+
+
+def _tag(tool, which, env):
+    return f"{tool}_{which}_" + ("_".join(f"{k}{v}" for k, v in env.items()) or "default")
+
+
+def _run_one(tool, which, env):
     out_dir = os.path.join(ROOT, "gpurun_out", "sanitizer")
     os.makedirs(out_dir, exist_ok=True)
-    tag = f"{tool}_{which}_" + ("_".join(f"{k}{v}" for k, v in env.items()) or "default")
-    log = os.path.join(out_dir, tag + ".txt")
+    log = os.path.join(out_dir, _tag(tool, which, env) + ".txt")
     cmd = [SANITIZER, "--tool", tool, "--error-exitcode", "99", "--log-file", log]
     if tool == "racecheck":
         cmd += ["--racecheck-report", "all"]
     cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_workload.py"), which]
-    r = subprocess.run(cmd, cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    r = subprocess.run(cmd, cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True, timeout=1200)
     report = open(log).read() if os.path.exists(log) else ""
-    assert f"sanitize workload {which} ok" in r.stdout, (r.stdout[-1000:], r.stderr[-2000:])
+    return r.returncode, r.stdout, r.stderr, report
+
+
+@pytest.fixture(scope="module")
+def sanitizer_runs():
+    """Every (tool, workload) run, several at a time: each is a separate small
+    process on the GPU, and running them concurrently keeps this suite's wall
+    time a fraction of running them one by one."""
+    if not os.path.exists(SANITIZER):
+        pytest.skip("compute-sanitizer not installed")
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = [(t, w, e) for t in TOOLS for w, e in CASES]
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        futs = {_tag(t, w, e): ex.submit(_run_one, t, w, e) for t, w, e in jobs}
+        return {k: f.result() for k, f in futs.items()}
+
+
+@pytest.mark.parametrize("tool", TOOLS)
+@pytest.mark.parametrize("which,env", CASES, ids=[f"{w}-{'-'.join(f'{k}={v}' for k, v in e.items()) or 'default'}"
+                                                  for w, e in CASES])
+def test_compute_sanitizer_clean(sanitizer_runs, tool, which, env):
+    rc, stdout, stderr, report = sanitizer_runs[_tag(tool, which, env)]
+    assert f"sanitize workload {which} ok" in stdout, (stdout[-1000:], stderr[-2000:])
     hazards = [h for h in re.split(r"\n(?==+ Error: )", report) if "Error: " in h]
     if tool == "racecheck" and which in ("gemm", "epi") and not env:
         # The CTA-pair kernel's only reports are "(CUDA barrier operation)"
@@ -51,7 +74,7 @@ def test_compute_sanitizer_clean(tool, which, env):
         own = [h for h in hazards if not _reserved_window_hazard(h)]
         assert not own, own[:3]
         return
-    assert r.returncode == 0, (r.returncode, report[-3000:], r.stdout[-1000:], r.stderr[-1000:])
+    assert rc == 0, (rc, report[-3000:], stdout[-1000:], stderr[-1000:])
     assert not hazards, hazards[:3]
     # the summary line must say zero (racecheck: "0 hazards displayed (0 errors, ...)")
     assert "SUMMARY" in report and ("0 errors" in report or "0 hazards" in report), report[-3000:]
