@@ -57,6 +57,14 @@ template <int kOut>
 __host__ __device__ constexpr int epi_warps() { return (kOut == 3 || COAT_GEMM_EPI8_ALL) ? 8 : 4; }
 template <int kOut>
 __host__ __device__ constexpr int threads_for() { return 64 + 32 * epi_warps<kOut>(); }
+// fp32 epilogue through a per-warp shared-memory tile (coalesced row stores)
+#ifndef COAT_GEMM_COALESCED
+#define COAT_GEMM_COALESCED 1
+#endif
+template <int kOut>
+__host__ __device__ constexpr int epi_smem_bytes() {
+    return (kOut == 0 && COAT_GEMM_COALESCED) ? epi_warps<kOut>() * 32 * 36 * 4 : 0;
+}
 constexpr int ACC_COLS = BN;              // fp32 columns per accumulator
 constexpr int TMEM_COLS = 2 * ACC_COLS;   // double buffer = all 512 columns
 
@@ -414,6 +422,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const int q = warp & 3;                    // TMEM lane quarter this warp may access
         const int half = epi_warps<kOut>() == 8 ? (warp - 2) >> 2 : 0;   // 8 warps: which column half
         const int row_in_tile = int(rank) * BM + q * 32 + lane;
+        // kOutF32: this warp's 32 x 36-float staging tile behind the barriers
+        float* stile = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * (32 * 36);
         const uint32_t tempty_leader0 = kCta == 2 ? cluster_addr(&tempty[0], 0) : 0u;
         float alpha = P.alpha;
         if (P.scale_a) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_a));
@@ -429,6 +439,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = mb * G::TILE_M + row_in_tile;
+            const int row_base = row - lane;   // the warp's first accumulator row
             const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * ACC_COLS);
             if (kOut == kOutUpGate) {
                 // accumulator columns [0, 128): gate, [128, 256): up, of output columns nb*128 + j
@@ -507,6 +518,25 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                         bad |= quant16_store(y, P.q.c0 + rq * P.q.ldc + col, P.q.s0 + rq * (P.q.ldc >> 4) + (col >> 4),
                                              -0.0f, live) & (live ? 1u : 0u);
                     }
+                } else if (kOut == kOutF32 && COAT_GEMM_COALESCED && col0 + 32 <= P.N && row_base + 32 <= P.M) {
+                    // the warp's 32 rows x 32 columns through a padded shared-memory
+                    // tile, so every store instruction writes 4 whole 128-byte row
+                    // segments instead of one 16-byte piece of 32 different rows
+                    // (row stride 36 floats: both access patterns bank-conflict free)
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        *reinterpret_cast<float4*>(stile + lane * 36 + i) =
+                            make_float4(__fmul_rn(alpha, u2f(r[i])), __fmul_rn(alpha, u2f(r[i + 1])),
+                                        __fmul_rn(alpha, u2f(r[i + 2])), __fmul_rn(alpha, u2f(r[i + 3])));
+                    __syncwarp();
+                    float* o = static_cast<float*>(P.out) + int64_t(row_base) * P.ldo + col0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int rr = 4 * j + (lane >> 3), cc = (lane & 7) * 4;
+                        *reinterpret_cast<float4*>(o + int64_t(rr) * P.ldo + cc) =
+                            *reinterpret_cast<const float4*>(stile + rr * 36 + cc);
+                    }
+                    __syncwarp();
                 } else if (row < P.M) {
                     if (kOut == kOutF32) {
                         float* o = static_cast<float*>(P.out) + int64_t(row) * P.ldo + col0;
@@ -622,7 +652,8 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     int dev = 0;
     cudaGetDevice(&dev);
     if (attr_dev != dev) {
-        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   G::SMEM_BYTES + epi_smem_bytes<kOut>());
         if (e != cudaSuccess) return e;
         attr_dev = dev;
     }
@@ -643,13 +674,13 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     const int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
     const int grid = kCta * (ntiles < units ? ntiles : units);
     if (kCta == 1) {
-        kern<<<grid, threads_for<kOut>(), G::SMEM_BYTES, stream>>>(ma, mb, mb2, P);
+        kern<<<grid, threads_for<kOut>(), G::SMEM_BYTES + epi_smem_bytes<kOut>(), stream>>>(ma, mb, mb2, P);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads_for<kOut>());
-    cfg.dynamicSmemBytes = G::SMEM_BYTES;
+    cfg.dynamicSmemBytes = G::SMEM_BYTES + epi_smem_bytes<kOut>();
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
