@@ -180,6 +180,26 @@ def test_quantize_batch_cooperative_kernel_matches_single_calls():
     assert "passed" in r.stdout
 
 
+def test_quantize_batch_llama_layer_matches_single_calls(coat):
+    """The nine MGAQ records of a Llama-2-7B layer (cfg2: 8192 tokens, H 4096,
+    I 11008; per-group 1x16 and per-tensor) in one coat_quantize_batch call,
+    bit-identical to the per-tensor entry points record by record."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(21)
+    specs = [((8192, 4096), 16), ((8192, 4096), 0), ((8192, 4096), 0), ((8192, 4096), 16), ((8192, 4096), 0),
+             ((8192, 11008), 16), ((8192, 11008), 16), ((8192, 11008), 16), ((8192, 11008), 0)]
+    xs = []
+    for shape, G in specs:
+        x = torch.randn(shape, device="cuda", generator=g) * 2
+        x[::100] *= 50
+        xs.append((x.to(torch.bfloat16), coat.QuantGeometry.per_group(G) if G else coat.QuantGeometry.per_tensor()))
+    batch = coat.quantize_batch(xs)
+    for (x, geo), qb in zip(xs, batch):
+        q = coat.quantize(x, geo)
+        assert torch.equal(q.codes, qb.codes)
+        assert torch.equal(q.scales.view(torch.int16), qb.scales.view(torch.int16))
+
+
 def test_quantize_batch_matches_single_calls(coat):
     """coat_quantize_batch (a layer's MGAQ records in one call: 3 internal
     streams by default) is bit-identical to the per-tensor entry points, mixed
