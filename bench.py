@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-extra", action="store_true",
                     help="default run: skip the cfg1 / cfg2 / cfg4 measurements added under `extra`")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="parameters per host-pipeline chunk of the N = 1 e2e step (0: the library default)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--mgaq-branches", type=int, default=3,
                     help="graph impl: records spread over this many parallel graph branches")
@@ -608,7 +610,7 @@ def run_e2e(args, L, _lib, P, n, ws, rank, w, g, w_full, g_full, g_shard, w_scra
             s = L.coat_adamw_dre_step_host(w_h.data_ptr(), w_h.data_ptr(), g_h.data_ptr(), n, GROUP,
                                            _cstate(_lib, m[i]), _cstate(_lib, v[i]), _cstate(_lib, m[1 - i]),
                                            _cstate(_lib, v[1 - i]), C.byref(cfg), t_step[0], flags.data_ptr(),
-                                           0, stream.cuda_stream)
+                                           args.e2e_chunk, stream.cuda_stream)
         else:
             shard = w_full[rank * n:(rank + 1) * n]
             g_full.copy_(g_h, non_blocking=True)
