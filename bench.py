@@ -862,8 +862,8 @@ def run_mgaq(args, extra_mode=False):
     def batch_step():
         st = L.coat_quantize_batch(items, len(bufs), flags.data_ptr(), torch.cuda.current_stream().cuda_stream)
         assert st == 0, L.coat_last_error()
-        if os.environ.get("COAT_MGAQ_BATCH", "").startswith("c"):
-            return 2   # memset of the grid-barrier word + the cooperative kernel
+        if os.environ.get("COAT_MGAQ_BATCH", "").startswith(("c", "q")):
+            return 2   # memset of the workspace + the one kernel
         return sum(1 if G else 3 for _, _, _, G in MGAQ_TENSORS)   # per record: kernel(s) (+ memset)
 
     for _ in range(args.warmup):
@@ -949,8 +949,10 @@ def run_mgaq(args, extra_mode=False):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16->e4m3", "data": "synthetic",
         "config": {"workload": "cfg2: MGAQ of one Llama-2-7B decoder layer, B4 x S2048 x H4096, I=11008",
-                   "impl": ("coat_quantize_batch (" + ("1 cooperative launch" if os.environ.get(
-                       "COAT_MGAQ_BATCH", "").startswith("c") else "3 internal streams") + ")")
+                   "impl": ("coat_quantize_batch (" + (
+                       "1 cooperative launch" if os.environ.get("COAT_MGAQ_BATCH", "").startswith("c") else
+                       "1 persistent task-queue launch" if os.environ.get("COAT_MGAQ_BATCH", "").startswith("q")
+                       else "3 internal streams") + ")")
                            if args.mgaq_impl == "batch"
                            else f"9 entry points as one CUDA graph, {args.mgaq_branches} parallel branch(es)",
                    "tensors": [t[:4] for t in MGAQ_TENSORS], "elements": nel,

@@ -140,21 +140,6 @@ dequant_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ s
 // Stage 1: per-1xG absmax -> intermediate (optional).  Stage 2: global max via
 // a block max + one atomicMax per CTA on the fp32 bit pattern.
 //
-// The per-tensor encode that follows reads x again; the amax pass marks the
-// LAST kL2KeepBytes of x L2::evict_last (the rest evict_first) and the encode
-// pass walks the chunks in reverse, so the resident tail is consumed first: a
-// tensor up to the budget is read from DRAM once, a larger one (down.in,
-// 180 MB > the 126 MB L2) re-reads only its head instead of all of it.
-// COAT_L2_KEEP_MB overrides the budget (A/B measurements).
-int64_t l2_keep_chunks(int64_t nchunks, int esz) {
-    static const int64_t keep_bytes = [] {
-        const char* e = getenv("COAT_L2_KEEP_MB");
-        return (e && *e ? int64_t(atoi(e)) : int64_t(80)) << 20;
-    }();
-    const int64_t keep = keep_bytes / (16 * esz);
-    return nchunks > keep ? nchunks - keep : 0;   // first chunk kept resident
-}
-
 template <int DT, int L>
 __global__ void __launch_bounds__(kThreads)
 group_amax_kernel(const void* __restrict__ x, int64_t nchunks, float* __restrict__ inter,
@@ -286,6 +271,21 @@ static bool pow2_lanes(int64_t G, int* L) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 static bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }   // 256-bit loads
+
+// The per-tensor encode that follows reads x again; the amax pass marks the
+// LAST kL2KeepBytes of x L2::evict_last (the rest evict_first) and the encode
+// pass walks the chunks in reverse, so the resident tail is consumed first: a
+// tensor up to the budget is read from DRAM once, a larger one (down.in,
+// 180 MB > the 126 MB L2) re-reads only its head instead of all of it.
+// COAT_L2_KEEP_MB overrides the budget (A/B measurements).
+int64_t l2_keep_chunks(int64_t nchunks, int esz) {
+    static const int64_t keep_bytes = [] {
+        const char* e = getenv("COAT_L2_KEEP_MB");
+        return (e && *e ? int64_t(atoi(e)) : int64_t(80)) << 20;
+    }();
+    const int64_t keep = keep_bytes / (16 * esz);
+    return nchunks > keep ? nchunks - keep : 0;   // first chunk kept resident
+}
 
 cudaError_t launch_quantize_per_group(const void* x, int dtype, int64_t n, int64_t G, uint8_t* codes,
                                       uint16_t* scales, uint32_t* flags, cudaStream_t st) {

@@ -168,7 +168,8 @@ coat_status coat_quantize_batch(const coat_mgaq_item* items, int32_t n_items, ui
         it[i] = MgaqItem{m.x, (int)m.dtype, n, G, m.codes, m.scales, m.d_amax_bits};
     }
     return cuda_status(mgaq_batch_cooperative() ? launch_mgaq_batch(it, n_items, d_flags, S(stream))
-                                                : launch_mgaq_streams(it, n_items, d_flags, S(stream)));
+                       : mgaq_batch_queue()    ? launch_mgaq_queue(it, n_items, d_flags, S(stream))
+                                               : launch_mgaq_streams(it, n_items, d_flags, S(stream)));
 }
 
 // ------------------------------------------------------- fused producers -----

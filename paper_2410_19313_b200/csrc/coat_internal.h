@@ -132,7 +132,12 @@ struct MgaqItem {
 };
 cudaError_t launch_mgaq_batch(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t stream);
 cudaError_t launch_mgaq_streams(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t stream);
+cudaError_t launch_mgaq_queue(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t stream);
 bool mgaq_batch_cooperative();
+bool mgaq_batch_queue();
+// first 16-element chunk of a per-tensor input kept L2-resident between its
+// absmax and encode passes (act_quant.cu; COAT_L2_KEEP_MB)
+int64_t l2_keep_chunks(int64_t nchunks, int esz);
 
 // fused producers (producers.cu)
 struct RmsBlockArgs {

@@ -20,7 +20,10 @@
 //            still in L2), each CTA reducing the item's partial maxima.
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
+#include <climits>
 #include <mutex>
+#include <vector>
 
 #include "act_quant.cuh"
 #include "coat_device.cuh"
@@ -236,6 +239,316 @@ cudaError_t launch_mgaq_batch(const MgaqItem* items, int n, uint32_t* flags, cud
 }
 
 // ---------------------------------------------------------------------------
+// The task-queue schedule (COAT_MGAQ_BATCH=queue): ONE persistent,
+// warp-specialised kernel for a whole layer.  A producer warp per CTA claims
+// tasks (32 KB of one record's input; two per atomic) from a global counter
+// and bulk-copies them (cp.async.bulk + mbarrier, with the L2 eviction hint)
+// into a ring of kSlots shared-memory slots; eight consumer warps quantize
+// slot after slot.  The host orders the queue so that every per-tensor
+// record's encode tasks come 2 (kSlots + kClaim) grids of per-group work after its
+// absmax tasks: the record's x is still in L2 (the absmax copies mark the tail
+// evict_last, the encode walks it tail first) and its absmax is complete.  The
+// producer of an encode task waits for the record's absmax-task count before
+// handing the slot over; every task it waits for was claimed earlier, and each
+// CTA processes its tasks in claim order while absmax tasks never wait, so the
+// queue cannot deadlock -- whether or not the whole grid is resident.
+// Specialised on the dtype, per-group items 1x16 (the cfg2 layer); other
+// batches take the stream schedule.
+namespace {
+#ifndef COAT_QUEUE_TASK_KB
+#define COAT_QUEUE_TASK_KB 32
+#endif
+#ifndef COAT_QUEUE_SLOTS
+#define COAT_QUEUE_SLOTS 3
+#endif
+#ifndef COAT_QUEUE_CLAIM
+#define COAT_QUEUE_CLAIM 2
+#endif
+constexpr int kTaskBytes = COAT_QUEUE_TASK_KB * 1024;
+constexpr int kSlots = COAT_QUEUE_SLOTS;
+constexpr int kClaim = COAT_QUEUE_CLAIM;        // tasks per atomic claim
+#ifndef COAT_QUEUE_MARGIN
+#define COAT_QUEUE_MARGIN 2                     // filler between a record's absmax and encode tasks, in lookaheads
+#endif
+#ifndef COAT_QUEUE_CONSUMERS
+#define COAT_QUEUE_CONSUMERS 256
+#endif
+constexpr int kConsumers = COAT_QUEUE_CONSUMERS;   // consumer threads (8 warps)
+constexpr int kQThreads = kConsumers + 32;      // + the producer warp
+constexpr int kMaxSegs = 3 * kMgaqMaxItems + 2;
+struct QSeg {
+    int64_t first_task;
+    int64_t chunk0, nchunks;        // chunks [chunk0, chunk0 + nchunks) of the item (encode: counted from its end)
+    int32_t item;
+    int32_t phase;                  // 0 per-group, 1 absmax, 2 encode
+};
+struct QParams {
+    BItem it[kMgaqMaxItems];
+    int64_t keep_from[kMgaqMaxItems];   // first chunk of the item's L2-resident tail
+    int32_t amax_tasks[kMgaqMaxItems];
+    QSeg seg[kMaxSegs];
+    int32_t nseg;
+    int64_t ntasks;
+    unsigned long long* counter;
+    uint32_t* amax;
+    uint32_t* done;
+    uint32_t* flags;
+};
+struct SlotMeta {
+    int64_t c0, c1;                 // chunk range; c0 < 0: no more tasks
+    int32_t item, phase;
+    float sc, rs;                   // encode: the record's scale and RN(1/scale)
+};
+
+template <int DT>
+__host__ __device__ constexpr int task_chunks() { return kTaskBytes / (16 * (DT == 0 ? 4 : 2)); }
+
+__device__ __forceinline__ uint32_t q_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void q_mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(q_smem(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void q_mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(q_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void q_mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(q_smem(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int DT>
+__device__ __forceinline__ RawChunk<DT> q_chunk(const uint8_t* buf, int64_t local) {
+    RawChunk<DT> c;
+    const uint4* p = reinterpret_cast<const uint4*>(buf + local * 16 * (DT == 0 ? 4 : 2));
+#pragma unroll
+    for (int k = 0; k < (DT == 0 ? 4 : 2); ++k) {
+        const uint4 v = p[k];
+        c.w[4 * k] = v.x; c.w[4 * k + 1] = v.y; c.w[4 * k + 2] = v.z; c.w[4 * k + 3] = v.w;
+    }
+    return c;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kQThreads) mgaq_queue_kernel(const __grid_constant__ QParams P, float nz) {
+    extern __shared__ __align__(128) uint8_t qsmem[];
+    __shared__ __align__(8) uint64_t full[kSlots], empty[kSlots];
+    __shared__ SlotMeta meta[kSlots];
+    __shared__ uint32_t s_red[kConsumers / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kSlots; ++i) {
+            q_mbar_init(&full[i], 1);
+            q_mbar_init(&empty[i], kConsumers / 32);   // one arrival per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int esz = DT == 0 ? 4 : 2;
+    if (warp == kConsumers / 32) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            long long t = 0, t_end = 0;   // claimed tasks [t, t_end)
+            int sgi = 0;                   // segment of the last task (claims only grow: the scan resumes)
+            for (int k = 0, slot = 0;; ++k, slot = (slot + 1) % kSlots) {
+                if (k >= kSlots) q_mbar_wait(&empty[slot], ((k / kSlots) - 1) & 1u);
+                if (t == t_end) {
+                    t = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
+                    t_end = t + kClaim;
+                }
+                SlotMeta& m = meta[slot];
+                if (t >= P.ntasks) {
+                    m.c0 = -1;
+                    q_mbar_arrive(&full[slot]);   // the end marker: consumers leave
+                    break;
+                }
+                const int64_t task = t++;
+                while (sgi + 1 < P.nseg && P.seg[sgi + 1].first_task <= task) ++sgi;
+                const QSeg& sg = P.seg[sgi];
+                const BItem& I = P.it[sg.item];
+                const int64_t a = sg.chunk0 + (task - sg.first_task) * task_chunks<DT>();
+                const int64_t e = sg.chunk0 + sg.nchunks;
+                const int64_t b = a + task_chunks<DT>() < e ? a + task_chunks<DT>() : e;
+                m.item = sg.item;
+                m.phase = sg.phase;
+                if (sg.phase == 2) {   // encode walks the tensor from its end
+                    m.c0 = I.nchunks - b;
+                    m.c1 = I.nchunks - a;
+                    while (ld_acquire_u32(&P.done[sg.item]) < uint32_t(P.amax_tasks[sg.item])) __nanosleep(64);
+                    const uint32_t am = ld_acquire_u32(&P.amax[sg.item]);
+                    const float sc = group_scale(u2f(am));
+                    m.sc = sc;
+                    m.rs = __frcp_rn(sc);
+                    if (task == sg.first_task) {   // the record's first encode task publishes scale and absmax
+                        I.scales[0] = float_to_bf16_bits_exact(sc);
+                        if (I.amax_out) *I.amax_out = am;
+                    }
+                } else {
+                    m.c0 = a;
+                    m.c1 = b;
+                }
+                uint64_t pol;
+                if (sg.phase == 1 && m.c1 > P.keep_from[sg.item])
+                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                else
+                    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                const uint32_t bytes = uint32_t((m.c1 - m.c0) * 16 * esz);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(q_smem(&full[slot])),
+                             "r"(bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+                    "%2, [%3], %4;" ::"r"(q_smem(qsmem + slot * kTaskBytes)),
+                    "l"(static_cast<const uint8_t*>(I.x) + m.c0 * 16 * esz), "r"(bytes), "r"(q_smem(&full[slot])),
+                    "l"(pol)
+                    : "memory");
+            }
+        }
+        return;
+    }
+    // ---------------------------------------------------------------- consumers
+    uint32_t bad = 0;
+    for (int k = 0, slot = 0;; ++k, slot = (slot + 1) % kSlots) {
+        q_mbar_wait(&full[slot], (k / kSlots) & 1u);
+        const SlotMeta m = meta[slot];
+        if (m.c0 < 0) break;
+        const BItem& I = P.it[m.item];
+        const uint8_t* buf = qsmem + slot * kTaskBytes;
+        const int64_t n = m.c1 - m.c0;
+        uint32_t am = 0;
+        for (int64_t j = threadIdx.x; j < n; j += kConsumers) {
+            const RawChunk<DT> raw = q_chunk<DT>(buf, j);
+            const int64_t ch = m.c0 + j;
+            if (m.phase == 0) {   // 1x16: one chunk = one group
+                const uint32_t ga = absmax_raw<DT, false>(raw);
+                float sc, rs;
+                group_scale_fast(ga, sc, rs);
+                reinterpret_cast<uint4*>(I.codes)[ch] = encode16(widen16<DT>(raw), sc, rs, nz);
+                I.scales[ch] = float_to_bf16_bits_exact(sc);
+                bad |= ga >= 0x7F800000u;
+            } else if (m.phase == 1) {
+                am = max(am, absmax_raw<DT, true>(raw));
+            } else {
+                reinterpret_cast<uint4*>(I.codes)[ch] = encode16(widen16<DT>(raw), m.sc, m.rs, nz);
+                bad |= absmax_raw<DT, false>(raw) >= 0x7F800000u;
+            }
+        }
+        if (m.phase == 1) {   // the task's absmax: consumer-only named barrier, one atomic per task
+            am = warp_max_u32(am);
+            if (lane == 0) s_red[warp] = am;
+            asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");
+            if (threadIdx.x == 0) {
+                uint32_t a = 0;
+                for (int w = 0; w < kConsumers / 32; ++w) a = max(a, s_red[w]);
+                if (a) atomicMax(&P.amax[m.item], a);
+                __threadfence();                       // the max before the count
+                atomicAdd(&P.done[m.item], 1u);
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(kConsumers) : "memory");   // s_red reusable
+        }
+        __syncwarp();
+        if (lane == 0) q_mbar_arrive(&empty[slot]);   // the slot's reads are done
+    }
+    if (P.flags && __reduce_or_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(P.flags, kFlagNonFiniteInput);
+}
+}  // namespace
+
+cudaError_t launch_mgaq_queue(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (n > kMgaqMaxItems) return cudaErrorInvalidValue;
+    const int dt = items[0].dtype;
+    for (int i = 0; i < n; ++i)
+        if (items[i].dtype != dt || (items[i].group_size != 0 && items[i].group_size != 16))
+            return launch_mgaq_streams(items, n, flags, st);   // the kernel's specialisation does not apply
+    const int smem = kSlots * kTaskBytes;
+    static int per_sm[2] = {0, 0};
+    static int occ_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (occ_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(mgaq_queue_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(mgaq_queue_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], mgaq_queue_kernel<0>, kQThreads, smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], mgaq_queue_kernel<1>, kQThreads, smem);
+        if (e != cudaSuccess) return e;
+        occ_dev = dev;
+    }
+    const int grid = device_sm_count() * (per_sm[dt] > 0 ? per_sm[dt] : 1);
+    const int64_t tc = dt == 0 ? task_chunks<0>() : task_chunks<1>();
+    QParams P{};
+    std::vector<int> pt, pg;
+    for (int i = 0; i < n; ++i) {
+        const MgaqItem& m = items[i];
+        BItem& b = P.it[i];
+        b.x = m.x;
+        b.codes = m.codes;
+        b.scales = m.scales;
+        b.amax_out = m.amax_out;
+        b.nchunks = m.n / 16;
+        b.dtype = m.dtype;
+        b.lanes = m.group_size ? 1 : 0;
+        P.keep_from[i] = l2_keep_chunks(b.nchunks, dt == 0 ? 4 : 2);
+        P.amax_tasks[i] = int32_t((b.nchunks + tc - 1) / tc);
+        (m.group_size ? pg : pt).push_back(i);
+    }
+    // queue: for every per-tensor record: its absmax tasks, twice kSlots + kClaim
+    // grids of per-group tasks (every CTA holds at most kSlots + kClaim claimed
+    // tasks, so the absmax tasks are processed well before), its encode
+    // tasks; then the rest of the per-group work
+    int64_t task = 0;
+    size_t gi = 0;          // current per-group item
+    int64_t gchunk = 0;     // its next chunk
+    auto add = [&](int item, int phase, int64_t c0, int64_t nch) {
+        QSeg& q = P.seg[P.nseg++];
+        q.first_task = task;
+        q.chunk0 = c0;
+        q.nchunks = nch;
+        q.item = item;
+        q.phase = phase;
+        task += (nch + tc - 1) / tc;
+    };
+    auto filler = [&](int64_t want_tasks) {
+        while (want_tasks > 0 && gi < pg.size() && P.nseg < kMaxSegs - 2) {
+            const BItem& b = P.it[pg[gi]];
+            const int64_t left = b.nchunks - gchunk;
+            const int64_t take = want_tasks >= (left + tc - 1) / tc ? left : want_tasks * tc;
+            add(pg[gi], 0, gchunk, take);
+            want_tasks -= (take + tc - 1) / tc;
+            gchunk += take;
+            if (gchunk >= b.nchunks) { ++gi; gchunk = 0; }
+        }
+    };
+    for (int i : pt) {
+        add(i, 1, 0, P.it[i].nchunks);
+        filler(int64_t(COAT_QUEUE_MARGIN) * (kSlots + kClaim) * grid);
+        add(i, 2, 0, P.it[i].nchunks);
+    }
+    filler(INT64_MAX);
+    P.ntasks = task;
+    P.flags = flags;
+    uint32_t* ws = nullptr;
+    const size_t wsb = (2 + 2 * kMgaqMaxItems) * sizeof(uint32_t);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), wsb, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(ws, 0, wsb, st);
+    if (e != cudaSuccess) return e;
+    P.counter = reinterpret_cast<unsigned long long*>(ws);
+    P.amax = ws + 2;
+    P.done = ws + 2 + kMgaqMaxItems;
+    if (dt == 0) mgaq_queue_kernel<0><<<grid, kQThreads, smem, st>>>(P, -0.0f);
+    else mgaq_queue_kernel<1><<<grid, kQThreads, smem, st>>>(P, -0.0f);
+    e = cudaGetLastError();
+    const cudaError_t f = cudaFreeAsync(ws, st);
+    return e != cudaSuccess ? e : f;
+}
+
+// ---------------------------------------------------------------------------
 // The default schedule of coat_quantize_batch: the records are independent, so
 // they are spread over 3 internal streams forked from (and joined back into)
 // the caller's stream, each record run by the same kernels as its per-tensor
@@ -263,6 +576,14 @@ bool mgaq_batch_cooperative() {
         return e && e[0] == 'c';
     }();
     return coop;
+}
+
+bool mgaq_batch_queue() {
+    static const bool q = [] {
+        const char* e = getenv("COAT_MGAQ_BATCH");
+        return e && e[0] == 'q';
+    }();
+    return q;
 }
 
 cudaError_t launch_mgaq_streams(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t st) {

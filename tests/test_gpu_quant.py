@@ -165,16 +165,19 @@ def test_llama_layer_sizes_bit_exact_full(coat, port):
     assert np.array_equal(host(qt.codes[sample]), exp)
 
 
-def test_quantize_batch_cooperative_kernel_matches_single_calls():
-    """The single cooperative launch behind COAT_MGAQ_BATCH=coop (chosen once
-    per process, hence a subprocess) gives the entry points' results too."""
+@pytest.mark.parametrize("mode", ["coop", "queue"])
+def test_quantize_batch_alternate_schedules_match_single_calls(mode):
+    """The single cooperative launch (COAT_MGAQ_BATCH=coop) and the persistent
+    warp-specialised task-queue kernel (=queue) behind coat_quantize_batch --
+    chosen once per process, hence a subprocess -- give the entry points'
+    results too, incl. the full Llama-2-7B layer."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, COAT_MGAQ_BATCH="coop")
+    env = dict(os.environ, COAT_MGAQ_BATCH=mode)
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_quant.py"), "-k", "batch and not cooperative"],
+                        os.path.join(here, "test_gpu_quant.py"), "-k", "batch and not alternate"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "passed" in r.stdout
