@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 SANITIZER = "/usr/local/cuda/bin/compute-sanitizer"
 CASES = [("k1", {"COAT_K1_EW": "8"}), ("k1", {"COAT_K1_EW": "7"}), ("k1", {"COAT_K1_EW": "6"}),
-         ("mgaq", {}), ("mgaq", {"COAT_MGAQ_BATCH": "coop"}),
+         ("mgaq", {}), ("mgaq", {"COAT_MGAQ_BATCH": "coop"}), ("mgaq16", {"COAT_MGAQ_BATCH": "queue"}),
          ("gemm", {}), ("gemm", {"COAT_GEMM_CTA": "1"}), ("epi", {}), ("epi", {"COAT_GEMM_CTA": "1"}),
          ("p2p", {})]
 

@@ -6,6 +6,8 @@ family, for `compute-sanitizer --tool racecheck|synccheck|memcheck`
          the environment) over several rounds per CTA + a ragged tail
   mgaq   coat_quantize_batch over per-group and per-tensor records
          (COAT_MGAQ_BATCH selects the internal-stream or cooperative form)
+  mgaq16 coat_quantize_batch over bf16 per-group 1x16 and per-tensor records
+         (the shape the COAT_MGAQ_BATCH=queue task-queue kernel takes)
   gemm   the FP8 forward and the BF16 dgrad / wgrad (COAT_GEMM_CTA=1: the
          single-CTA kernel; default the CTA-pair kernel)
   epi    the quantizing GEMM epilogues: per-group 1x16 output and the fused
@@ -42,6 +44,14 @@ def main(which):
               (torch.randn(32, 512, device="cuda"), coat.QuantGeometry.per_tensor()),
               (torch.randn(48, 1024, device="cuda").to(torch.bfloat16), coat.QuantGeometry.per_tensor()),
               (torch.randn(16, 128, device="cuda"), coat.QuantGeometry.per_group(32))]
+        qs = coat.quantize_batch(xs)
+        torch.cuda.synchronize()
+        assert len(qs) == len(xs)
+    elif which == "mgaq16":
+        xs = [(torch.randn(64, 256, device="cuda").to(torch.bfloat16), coat.QuantGeometry.per_group(16)),
+              (torch.randn(96, 512, device="cuda").to(torch.bfloat16), coat.QuantGeometry.per_tensor()),
+              (torch.randn(48, 2048, device="cuda").to(torch.bfloat16), coat.QuantGeometry.per_group(16)),
+              (torch.randn(80, 1024, device="cuda").to(torch.bfloat16), coat.QuantGeometry.per_tensor())]
         qs = coat.quantize_batch(xs)
         torch.cuda.synchronize()
         assert len(qs) == len(xs)
