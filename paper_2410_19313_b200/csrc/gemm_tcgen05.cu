@@ -53,8 +53,13 @@ constexpr int THREADS = 192;
 #ifndef COAT_GEMM_EPI8_ALL
 #define COAT_GEMM_EPI8_ALL 0
 #endif
+#ifndef COAT_GEMM_UPGATE_EPI
+#define COAT_GEMM_UPGATE_EPI 16
+#endif
 template <int kOut>
-__host__ __device__ constexpr int epi_warps() { return (kOut == 3 || COAT_GEMM_EPI8_ALL) ? 8 : 4; }
+__host__ __device__ constexpr int epi_warps() {
+    return kOut == 3 ? COAT_GEMM_UPGATE_EPI : COAT_GEMM_EPI8_ALL ? 8 : 4;
+}
 template <int kOut>
 __host__ __device__ constexpr int threads_for() { return 64 + 32 * epi_warps<kOut>(); }
 // fp32 epilogue through a per-warp shared-memory tile (coalesced row stores)
@@ -217,6 +222,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -420,7 +432,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     } else {
         // ------------------------------------------------------ epilogue (warps 2 .. 1 + epi_warps)
         const int q = warp & 3;                    // TMEM lane quarter this warp may access
-        const int half = epi_warps<kOut>() == 8 ? (warp - 2) >> 2 : 0;   // 8 warps: which column half
+        const int half = (warp - 2) >> 2;          // which column part (epi_warps / 4 parts)
         const int row_in_tile = int(rank) * BM + q * 32 + lane;
         // kOutF32: this warp's 32 x 36-float staging tile behind the barriers
         float* stile = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * (32 * 36);
@@ -445,49 +457,46 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 // accumulator columns [0, 128): gate, [128, 256): up, of output columns nb*128 + j
                 const bool live = row < P.M;
                 const int64_t rq = live ? row : 0;
+                constexpr int kGroups = 8 * 4 / epi_warps<kOut>();   // 16-column groups per warp (of 8 per half)
 #pragma unroll 1
-                constexpr int kChunks = 16 / epi_warps<kOut>();   // 32-column chunks per warp (of 4)
-                for (int c = half * kChunks; c < (half + 1) * kChunks; ++c) {
-                    uint32_t rg[32], ru[32];
-                    tmem_ld32(taddr + uint32_t(c * 32), rg);
-                    tmem_ld32(taddr + uint32_t(128 + c * 32), ru);
+                for (int gi = half * kGroups; gi < (half + 1) * kGroups; ++gi) {
+                    uint32_t rg[16], ru[16];
+                    tmem_ld16(taddr + uint32_t(gi * 16), rg);
+                    tmem_ld16(taddr + uint32_t(128 + gi * 16), ru);
                     tmem_wait_ld();
+                    const int col = nb * 128 + gi * 16;
+                    if (col >= P.N) break;   // warp-uniform (N % 16 == 0)
+                    aq::Chunk16 gv, uv;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int col = nb * 128 + c * 32 + h * 16;
-                        if (col >= P.N) break;   // warp-uniform (N % 16 == 0)
-                        aq::Chunk16 gv, uv;
+                    for (int i = 0; i < 16; ++i) {
+                        gv.v[i] = __fmul_rn(alpha, u2f(rg[i]));
+                        uv.v[i] = __fmul_rn(alpha_u, u2f(ru[i]));
+                    }
+                    if (live && P.q.y0) {
+                        float4* o = reinterpret_cast<float4*>(P.q.y0 + rq * P.q.ldc + col);
+                        float4* o1 = reinterpret_cast<float4*>(P.q.y1 + rq * P.q.ldc + col);
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            gv.v[i] = __fmul_rn(alpha, u2f(rg[16 * h + i]));
-                            uv.v[i] = __fmul_rn(alpha_u, u2f(ru[16 * h + i]));
+                        for (int k = 0; k < 4; ++k) {
+                            o[k] = make_float4(gv.v[4 * k], gv.v[4 * k + 1], gv.v[4 * k + 2], gv.v[4 * k + 3]);
+                            o1[k] = make_float4(uv.v[4 * k], uv.v[4 * k + 1], uv.v[4 * k + 2], uv.v[4 * k + 3]);
                         }
-                        if (live && P.q.y0) {
-                            float4* o = reinterpret_cast<float4*>(P.q.y0 + rq * P.q.ldc + col);
-                            float4* o1 = reinterpret_cast<float4*>(P.q.y1 + rq * P.q.ldc + col);
+                    }
+                    const int64_t co = rq * P.q.ldc + col, so = rq * (P.q.ldc >> 4) + (col >> 4);
+                    uint4 cw;
+                    uint16_t sbits;
+                    float gam;
+                    bad |= aq::quant_dq16(gv, cw, sbits, -0.0f, &gam);   // silu.in
+                    if (live) { *reinterpret_cast<uint4*>(P.q.c0 + co) = cw; P.q.s0[so] = sbits; }
+                    aq::silu16(gv, -0.0f, gam);
+                    bad |= aq::quant_dq16(gv, cw, sbits, -0.0f);   // mul.in.silu
+                    if (live) { *reinterpret_cast<uint4*>(P.q.c1 + co) = cw; P.q.s1[so] = sbits; }
+                    bad |= aq::quant_dq16(uv, cw, sbits, -0.0f);   // mul.in.up
+                    if (live) { *reinterpret_cast<uint4*>(P.q.c2 + co) = cw; P.q.s2[so] = sbits; }
+                    if (live) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                o[k] = make_float4(gv.v[4 * k], gv.v[4 * k + 1], gv.v[4 * k + 2], gv.v[4 * k + 3]);
-                                o1[k] = make_float4(uv.v[4 * k], uv.v[4 * k + 1], uv.v[4 * k + 2], uv.v[4 * k + 3]);
-                            }
-                        }
-                        const int64_t co = rq * P.q.ldc + col, so = rq * (P.q.ldc >> 4) + (col >> 4);
-                        uint4 cw;
-                        uint16_t sbits;
-                        float gam;
-                        bad |= aq::quant_dq16(gv, cw, sbits, -0.0f, &gam);   // silu.in
-                        if (live) { *reinterpret_cast<uint4*>(P.q.c0 + co) = cw; P.q.s0[so] = sbits; }
-                        aq::silu16(gv, -0.0f, gam);
-                        bad |= aq::quant_dq16(gv, cw, sbits, -0.0f);   // mul.in.silu
-                        if (live) { *reinterpret_cast<uint4*>(P.q.c1 + co) = cw; P.q.s1[so] = sbits; }
-                        bad |= aq::quant_dq16(uv, cw, sbits, -0.0f);   // mul.in.up
-                        if (live) { *reinterpret_cast<uint4*>(P.q.c2 + co) = cw; P.q.s2[so] = sbits; }
-                        if (live) {
-#pragma unroll
-                            for (int i = 0; i < 16; i += 2) {
-                                const F2 pr = f2_mul(F2{gv.v[i], gv.v[i + 1]}, F2{uv.v[i], uv.v[i + 1]}, -0.0f);
-                                asm("max.f32 %0, %1, %2, %3;" : "=f"(amp) : "f"(amp), "f"(fabsf(pr.x)), "f"(fabsf(pr.y)));
-                            }
+                        for (int i = 0; i < 16; i += 2) {
+                            const F2 pr = f2_mul(F2{gv.v[i], gv.v[i + 1]}, F2{uv.v[i], uv.v[i + 1]}, -0.0f);
+                            asm("max.f32 %0, %1, %2, %3;" : "=f"(amp) : "f"(amp), "f"(fabsf(pr.x)), "f"(fabsf(pr.y)));
                         }
                     }
                 }
