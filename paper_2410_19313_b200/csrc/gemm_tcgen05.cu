@@ -46,19 +46,17 @@ constexpr int BN = 256;                   // accumulator columns (MMA N)
 constexpr int BKB = 128;                  // K bytes per stage (one 128B swizzle row)
 constexpr int A_BYTES = BM * BKB;         // 16 KiB
 constexpr int THREADS = 192;
-// Epilogue warps: 4 (one per TMEM lane quarter) -- or 8 for the quantizing
+// Epilogue warps: 4 (one per TMEM lane quarter) -- or 16 for the quantizing
 // gate/up epilogue, whose per-element work (three quantizers + SiLU) is longer
-// than the MMA main loop of a tile with 4 warps (ncu: tensor pipe 62%); the
-// second four take the other half of the accumulator's columns.
-#ifndef COAT_GEMM_EPI8_ALL
-#define COAT_GEMM_EPI8_ALL 0
-#endif
+// than the MMA main loop of a tile with 4 warps (ncu: tensor pipe 62%); each
+// group of four takes a quarter of the accumulator's columns.  (8 warps for
+// the plain epilogues measured +-0.)
 #ifndef COAT_GEMM_UPGATE_EPI
 #define COAT_GEMM_UPGATE_EPI 16
 #endif
 template <int kOut>
 __host__ __device__ constexpr int epi_warps() {
-    return kOut == 3 ? COAT_GEMM_UPGATE_EPI : COAT_GEMM_EPI8_ALL ? 8 : 4;
+    return kOut == 3 ? COAT_GEMM_UPGATE_EPI : 4;
 }
 template <int kOut>
 __host__ __device__ constexpr int threads_for() { return 64 + 32 * epi_warps<kOut>(); }
