@@ -433,7 +433,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const int half = (warp - 2) >> 2;          // which column part (epi_warps / 4 parts)
         const int row_in_tile = int(rank) * BM + q * 32 + lane;
         // kOutF32: this warp's 32 x 36-float staging tile behind the barriers
-        float* stile = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * (32 * 36);
+        const uint32_t stile = smem_u32(smem + STAGES * STAGE_BYTES + 256) + uint32_t((warp - 2) * (32 * 36) * 4);
         const uint32_t tempty_leader0 = kCta == 2 ? cluster_addr(&tempty[0], 0) : 0u;
         float alpha = P.alpha;
         if (P.scale_a) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_a));
@@ -532,16 +532,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                     // (row stride 36 floats: both access patterns bank-conflict free)
 #pragma unroll
                     for (int i = 0; i < 32; i += 4)
-                        *reinterpret_cast<float4*>(stile + lane * 36 + i) =
-                            make_float4(__fmul_rn(alpha, u2f(r[i])), __fmul_rn(alpha, u2f(r[i + 1])),
-                                        __fmul_rn(alpha, u2f(r[i + 2])), __fmul_rn(alpha, u2f(r[i + 3])));
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stile + uint32_t((lane * 36 + i) * 4)),
+                                     "f"(__fmul_rn(alpha, u2f(r[i]))), "f"(__fmul_rn(alpha, u2f(r[i + 1]))),
+                                     "f"(__fmul_rn(alpha, u2f(r[i + 2]))), "f"(__fmul_rn(alpha, u2f(r[i + 3])))
+                                     : "memory");
                     __syncwarp();
                     float* o = static_cast<float*>(P.out) + int64_t(row_base) * P.ldo + col0;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int rr = 4 * j + (lane >> 3), cc = (lane & 7) * 4;
-                        *reinterpret_cast<float4*>(o + int64_t(rr) * P.ldo + cc) =
-                            *reinterpret_cast<const float4*>(stile + rr * 36 + cc);
+                        float4 v;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                                     : "r"(stile + uint32_t((rr * 36 + cc) * 4))
+                                     : "memory");
+                        *reinterpret_cast<float4*>(o + int64_t(rr) * P.ldo + cc) = v;
                     }
                     __syncwarp();
                 } else if (row < P.M) {
