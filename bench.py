@@ -1228,6 +1228,10 @@ def run_linear(args, extra_mode=False):
     cpu = None if args.no_cpu_baseline else linear_cpu_baseline()
     tf = {k: flop / (per[k] * 1e-3) / 1e12 for k in ("fwd", "dgrad", "wgrad")}
     upgate = mlp_upgate_compare(L, xc, sx, wc, sw, M, K, N, dev, st)
+    try:
+        library = library_same_shape(L, xc, sx, wc, sw, dy, wd, dx, y, M, K, N, st)
+    except Exception as ex:  # the comparison is informative only
+        library = {"error": f"{ex!r:.120}"}
     out = {
         "metric": "Per-tensor FP8 linear fwd+bwd (cfg4), TFLOP/s", "value": 3 * flop / (ms * 1e-3) / 1e12,
         "unit": "TFLOP/s", "n_gpus": 1, "steps": reps, "warmup": args.warmup, "ms_per_step": ms,
@@ -1244,8 +1248,51 @@ def run_linear(args, extra_mode=False):
                      "bwd_frac_of_bf16": {"dgrad": tf["dgrad"] / bf16_peak, "wgrad": tf["wgrad"] / bf16_peak},
                      "bf16_peak": bf16_peak, "bf16_peak_kind": bf16_kind},
         "cpu_baseline": cpu, "clocks": sampler.summary(), "gpu_launches": 9 * reps,
-        "mlp_upgate": upgate,
+        "mlp_upgate": upgate, "library_same_shape": library,
     }
+    return out
+
+
+def library_same_shape(L, xc, sx, wc, sw, dy, wd, dx, y, M, K, N, st):
+    """K4 against the library on cfg4's own shapes, timed interleaved (ours,
+    library, ours, library; >= 0.4 s each, best of the two) so both see the
+    same power / clock state: the FP8 forward against cuBLASLt's E4M3 GEMM with
+    fp32 output (torch._scaled_mm on the same codes), the BF16 dgrad against
+    cuBLAS (dy . Wd^T).  Timing only -- the library arms take unit scales."""
+    import torch
+    wt = wc.t().contiguous().view(torch.float8_e4m3fn)          # (N, K): mat2 column-major
+    a = xc.view(torch.float8_e4m3fn)
+    one = torch.ones((), device=xc.device)
+    dxl = torch.empty_like(dx)
+    s = st.cuda_stream
+    arms = {
+        "k4_fwd": lambda: L.coat_fp8_linear_fwd(xc.data_ptr(), sx.data_ptr(), wc.data_ptr(), sw.data_ptr(),
+                                                M, K, N, y.data_ptr(), s),
+        "cublaslt_fp8_fwd": lambda: torch._scaled_mm(a, wt.t(), scale_a=one, scale_b=one,
+                                                     out_dtype=torch.float32),
+        "k4_dgrad": lambda: L.coat_linear_bwd_dgrad(dy.data_ptr(), wd.data_ptr(), sw.data_ptr(), M, K, N,
+                                                    dx.data_ptr(), s),
+        "cublas_bf16_dgrad": lambda: torch.matmul(dy, wd.t(), out=dxl),
+    }
+    best = {}
+    for _ in range(2):
+        for name, fn in arms.items():
+            for _ in range(3):
+                fn()
+            reps = _reps_for(fn, 0.4, 5)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(reps):
+                fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            best[name] = min(best.get(name, 1e9), e0.elapsed_time(e1) / reps)
+    flop = 2.0 * M * N * K
+    out = {k + "_ms": v for k, v in best.items()}
+    out.update({"fwd_vs_cublaslt": best["cublaslt_fp8_fwd"] / best["k4_fwd"],
+                "dgrad_vs_cublas": best["cublas_bf16_dgrad"] / best["k4_dgrad"],
+                "tflops": {k: flop / (v * 1e-3) / 1e12 for k, v in best.items()},
+                "what": "interleaved best-of-2 >= 0.4 s loops; ratio > 1 means K4 is faster"})
     return out
 
 

@@ -71,16 +71,21 @@ __host__ __device__ constexpr int epi_smem_bytes() {
 constexpr int ACC_COLS = BN;              // fp32 columns per accumulator
 constexpr int TMEM_COLS = 2 * ACC_COLS;   // double buffer = all 512 columns
 
+// kCta: 1 = one CTA, 2 = a CTA pair, 4 = two CTA pairs in a cluster of 4 that
+// share the B tile (same N block, adjacent M blocks): each CTA loads half of
+// its B half and multicasts it to the same-rank CTA of the other pair, so the
+// L2 -> SM operand traffic per FLOP drops by another quarter.
 template <int kCta>
 struct Geo {
-    static constexpr int BN_L = BN / kCta;                 // B rows staged by this CTA
+    static constexpr int PAIR = kCta >= 2 ? 2 : 1;         // CTAs per MMA
+    static constexpr int BN_L = BN / PAIR;                 // B rows staged by this CTA
     static constexpr int B_BYTES = BN_L * BKB;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 #ifndef COAT_GEMM_PAIR_STAGES
 #define COAT_GEMM_PAIR_STAGES 6
 #endif
-    static constexpr int STAGES = kCta == 2 ? COAT_GEMM_PAIR_STAGES : 4;
-    static constexpr int TILE_M = BM * kCta;
+    static constexpr int STAGES = kCta >= 2 ? COAT_GEMM_PAIR_STAGES : 4;
+    static constexpr int TILE_M = BM * PAIR;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -115,6 +120,7 @@ struct EpiQ {
 struct Params {
     int M, N, K;               // K in elements
     int tiles_m, tiles_n, k_blocks;
+    int group_m;               // tile raster: groups of group_m M-blocks, M fastest inside a group
     float alpha;               // epilogue scale
     const uint16_t* scale_a;   // optional BF16 device scalars multiplied into alpha
     const uint16_t* scale_b;
@@ -122,6 +128,23 @@ struct Params {
     int64_t ldo;               // elements
     EpiQ q;
 };
+
+// Grouped raster of the persistent tile walk: tiles [g * group_m * tiles_n, ...)
+// cover M-blocks [g * group_m, +group_m) x every N-block, M fastest.  The
+// CTAs in flight at any moment then cover ~group_m M-blocks x (units /
+// group_m) N-blocks instead of every M-block of one or two N columns -- with a
+// long K (dgrad: 13824) a 256-row operand block is 7 MB, and the M-fastest
+// walk streamed all of dY from DRAM once per wave (ncu: 2.4 GB read vs
+// cuBLAS's 0.93 GB on the same shape, and the extra DRAM power cost ~12% of
+// the clock).
+__device__ __forceinline__ void tile_coords(const Params& P, int tile, int& mb, int& nb) {
+    const int span = P.group_m * P.tiles_n;
+    const int g = tile / span, r = tile - g * span;
+    const int m_first = g * P.group_m;
+    const int gm = min(P.tiles_m - m_first, P.group_m);
+    nb = r / gm;
+    mb = m_first + (r - nb * gm);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -135,6 +158,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef COAT_GEMM_DEBUG_WAIT
+// debug build: bounded waits that report the stuck barrier and trap
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    for (long long i = 0;; ++i) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (i == (1ll << 24)) {
+            uint32_t cr;
+            asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+            printf("stuck: block %d crank %u thread %d bar smem+%u parity %u\n", blockIdx.x, cr, threadIdx.x,
+                   smem_u32(bar), parity);
+            __trap();
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n.reg .pred p;\nW_%=:\n"
@@ -143,6 +187,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#endif
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -177,11 +222,24 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         "l"(map), "r"(x), "r"(y), "r"(bar_caddr)
         : "memory");
 }
-__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+// The same into the CTAs of `mask` (same smem offset in each); the completion
+// bytes land on the barrier of each destination's pair leader.  The mbarrier
+// operand is this CTA's own barrier address with the peer bit (bit 24 of a
+// shared-window address: the odd CTA of a pair) cleared -- without the mask an
+// odd CTA's bytes would count on its own barrier, which nobody waits on.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                                    uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask = 3) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
-        "h"(uint16_t(3))
+        "h"(mask)
         : "memory");
 }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -276,23 +334,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+#ifdef COAT_GEMM_DEBUG_WAIT
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("barriers: full %u empty %u tfull %u tempty %u (stages %d)\n", smem_u32(full), smem_u32(empty),
+               smem_u32(tfull), smem_u32(tempty), STAGES);
+#endif
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int ESZ = kF8 ? 1 : 2;
     constexpr int BK = BKB / ESZ;                  // K elements per stage
     constexpr int UK = 32 / ESZ;                   // K elements per MMA (32 bytes)
     const int ntiles = P.tiles_m * P.tiles_n;
-    const uint32_t rank = kCta == 2 ? cluster_rank() : 0u;
+    const uint32_t crank = kCta >= 2 ? cluster_rank() : 0u;
+    const uint32_t rank = crank & 1u;          // rank inside the CTA pair
+    const uint32_t pidx = crank >> 1;          // kCta 4: which pair of the cluster
     const int tile0 = blockIdx.x / kCta, tstep = gridDim.x / kCta;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], kCta == 4 ? 2 : 1);   // kCta 4: both pairs' MMAs read the B halves
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], epi_warps<kOut>() * kCta);   // one arrive per epilogue warp of the pair
+            mbar_init(&tempty[a], epi_warps<kOut>() * G::PAIR);   // one arrive per epilogue warp of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -314,7 +379,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
     }
     tc_fence_before();
-    if (kCta == 2) cluster_sync_all();   // barriers initialised in both CTAs before any remote use
+    if (kCta >= 2) cluster_sync_all();   // barriers initialised in every CTA before any remote use
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -325,7 +390,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = tile0; tile < ntiles; tile += tstep) {
-                const int mb = tile % P.tiles_m, nb = tile / P.tiles_m;
+                int mb, nb;
+                tile_coords(P, tile, mb, nb);
+                if (kCta == 4) mb = 2 * mb + int(pidx);
                 const int m0 = mb * G::TILE_M + int(rank) * BM;     // this CTA's A rows
                 const int n0 = nb * BN + int(rank) * G::BN_L;       // this CTA's B rows
                 for (int kb = 0; kb < P.k_blocks; ++kb) {
@@ -352,6 +419,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 #pragma unroll
                             for (int c = 0; c < G::BN_L * ESZ / 128; ++c)
                                 tma_load_2d(sb + c * BK * 128, &map_b, n0 + c * (128 / ESZ), k0, &full[stage]);
+                        }
+                    } else if (kCta == 4) {
+                        // the pair leader's full barrier counts both CTAs' bytes: own A rows,
+                        // B half = this CTA's quarter + the other pair's same-rank CTA's quarter
+                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                        const uint32_t fb = cluster_addr(&full[stage], crank & ~1u);
+                        const uint16_t mc = uint16_t((1u << rank) | (1u << (2 + rank)));
+                        if (!kAMN) {
+                            tma_load_2d_pair(sa, &map_a, k0, m0, fb);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < BM * ESZ / 128; ++c)
+                                tma_load_2d_pair(sa + c * BK * 128, &map_a, m0 + c * (128 / ESZ), k0, fb);
+                        }
+                        if (!kBMN) {
+                            constexpr int h = G::BN_L / 2;   // B rows per quarter
+                            tma_load_2d_pair_mc(sb + int(pidx) * h * 128, &map_b, k0, n0 + int(pidx) * h, &full[stage],
+                                                mc);
+                        } else {
+                            constexpr int h = BK / 2;        // K rows per quarter of each 128-byte column chunk
+#pragma unroll
+                            for (int c = 0; c < G::BN_L * ESZ / 128; ++c)
+                                tma_load_2d_pair_mc(sb + c * BK * 128 + int(pidx) * h * 128, &map_b,
+                                                    n0 + c * (128 / ESZ), k0 + int(pidx) * h, &full[stage], mc);
                         }
                     } else {
                         // the leader's full barrier counts both CTAs' bytes
@@ -412,7 +503,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                     }
                     // frees the smem stage (in both CTAs) when these MMAs retire
                     if (kCta == 1) tc_commit(&empty[stage]);
-                    else tc_commit_pair(&empty[stage]);
+                    else tc_commit_pair(&empty[stage], kCta == 4 ? uint16_t(0xF) : uint16_t(3));
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -420,7 +511,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 }
                 // accumulator ready for the epilogue(s)
                 if (kCta == 1) tc_commit(&tfull[acc]);
-                else tc_commit_pair(&tfull[acc]);
+                else tc_commit_pair(&tfull[acc], uint16_t(3u << (2 * pidx)));
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1u;
@@ -434,7 +525,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const int row_in_tile = int(rank) * BM + q * 32 + lane;
         // kOutF32: this warp's 32 x 36-float staging tile behind the barriers
         const uint32_t stile = smem_u32(smem + STAGES * STAGE_BYTES + 256) + uint32_t((warp - 2) * (32 * 36) * 4);
-        const uint32_t tempty_leader0 = kCta == 2 ? cluster_addr(&tempty[0], 0) : 0u;
+        const uint32_t tempty_leader0 = kCta >= 2 ? cluster_addr(&tempty[0], crank & ~1u) : 0u;
         float alpha = P.alpha;
         if (P.scale_a) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_a));
         float alpha_u = alpha;
@@ -445,7 +536,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = tile0; tile < ntiles; tile += tstep) {
-            const int mb = tile % P.tiles_m, nb = tile / P.tiles_m;
+            int mb, nb;
+            tile_coords(P, tile, mb, nb);
+            if (kCta == 4) mb = 2 * mb + int(pidx);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = mb * G::TILE_M + row_in_tile;
@@ -602,7 +695,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             atomicOr(P.q.flags, kFlagNonFiniteInput);
     }
     tc_fence_before();
-    if (kCta == 2) cluster_sync_all();   // no CTA of the pair leaves while the other may still signal it
+    if (kCta >= 2) cluster_sync_all();   // no CTA of the cluster leaves while another may still signal it
     else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
@@ -643,6 +736,39 @@ bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t c
     return r == CUDA_SUCCESS;
 }
 
+// Co-resident clusters of 4 (GPC boundaries leave some SMs out), cached per kernel.
+template <typename K>
+int max_clusters4(K kern, int smem, int threads) {
+    static int cached = -1;
+    if (cached < 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(4 * 64);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 4;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+        cached = n;
+    }
+    return cached;
+}
+
+// COAT_GEMM_GROUP_M overrides the raster group (A/B; 0 or >= tiles_m = the
+// plain M-fastest walk).
+inline int raster_group_m(int tiles_m) {
+    static const int v = [] {
+        const char* e = getenv("COAT_GEMM_GROUP_M");
+        return e ? atoi(e) : 8;
+    }();
+    return (v <= 0 || v > tiles_m) ? tiles_m : v;
+}
+
 template <bool kF8, bool kAMN, bool kBMN, int kOut, int kCta>
 cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, int K, float alpha,
                     const uint16_t* sa, const uint16_t* sb, void* out, int64_t ldo, const EpiQ& q,
@@ -653,8 +779,9 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     CUtensorMap ma, mb, mb2;
     // A logical [M x K]: K-major memory [M][K]; MN-major memory [K][M]
     const bool ok_a = !kAMN ? make_map(&ma, a, ESZ, M, K, BK, BM) : make_map(&ma, a, ESZ, K, M, 128 / ESZ, BK);
-    const bool ok_b =
-        !kBMN ? make_map(&mb, b, ESZ, N, K, BK, G::BN_L) : make_map(&mb, b, ESZ, K, N, 128 / ESZ, BK);
+    // kCta 4: the B box is a quarter (half of this CTA's half; see the producer)
+    const bool ok_b = !kBMN ? make_map(&mb, b, ESZ, N, K, BK, kCta == 4 ? G::BN_L / 2 : G::BN_L)
+                            : make_map(&mb, b, ESZ, K, N, 128 / ESZ, kCta == 4 ? BK / 2 : BK);
     // kOutUpGate: the up weight (same geometry as the gate weight); else a copy of B (unused)
     const bool ok_b2 = kOut == kOutUpGate ? make_map(&mb2, b2, ESZ, K, N, 128 / ESZ, BK) : true;
     if (!ok_a || !ok_b || !ok_b2) return cudaErrorInvalidValue;
@@ -674,8 +801,10 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     P.N = N;
     P.K = K;
     P.tiles_m = (M + G::TILE_M - 1) / G::TILE_M;
+    if (kCta == 4) P.tiles_m = (P.tiles_m + 1) / 2;   // super-blocks of two pair tiles (the odd one out is all OOB)
     P.tiles_n = kOut == kOutUpGate ? (N + 127) / 128 : (N + BN - 1) / BN;
     P.k_blocks = (K + BK - 1) / BK;
+    P.group_m = raster_group_m(P.tiles_m);
     P.alpha = alpha;
     P.scale_a = sa;
     P.scale_b = sb;
@@ -683,7 +812,9 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     P.ldo = ldo;
     P.q = q;
     const int ntiles = P.tiles_m * P.tiles_n;
-    const int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
+    int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
+    if (kCta == 4) units = max_clusters4(kern, G::SMEM_BYTES + epi_smem_bytes<kOut>(), threads_for<kOut>());
+    if (units <= 0) return cudaErrorInvalidConfiguration;
     const int grid = kCta * (ntiles < units ? ntiles : units);
     if (kCta == 1) {
         kern<<<grid, threads_for<kOut>(), G::SMEM_BYTES + epi_smem_bytes<kOut>(), stream>>>(ma, mb, mb2, P);
@@ -696,7 +827,7 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = kCta;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -704,11 +835,12 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     return cudaLaunchKernelEx(&cfg, kern, ma, mb, mb2, P);
 }
 
-// COAT_GEMM_CTA=1 forces the single-CTA kernel (A/B comparisons).
+// COAT_GEMM_CTA=1 forces the single-CTA kernel, =4 the two-pair B-multicast
+// cluster (A/B comparisons).
 inline int pair_mode() {
     static const int v = [] {
         const char* e = getenv("COAT_GEMM_CTA");
-        return (e && e[0] == '1') ? 1 : 2;
+        return (e && e[0] == '1') ? 1 : (e && e[0] == '4') ? 4 : 2;
     }();
     return v;
 }
@@ -717,7 +849,10 @@ template <bool kF8, bool kAMN, bool kBMN, int kOut>
 cudaError_t run(const void* a, const void* b, int M, int N, int K, float alpha, const uint16_t* sa,
                 const uint16_t* sb, void* out, int64_t ldo, cudaStream_t stream, const EpiQ& q = EpiQ{},
                 const void* b2 = nullptr) {
-    if (M > BM && pair_mode() == 2)
+    if (kOut != kOutUpGate && M > 2 * BM && pair_mode() == 4)
+        return run_cta<kF8, kAMN, kBMN, kOut == kOutUpGate ? kOutF32 : kOut, 4>(a, b, b2, M, N, K, alpha, sa, sb, out,
+                                                                              ldo, q, stream);
+    if (M > BM && pair_mode() >= 2)
         return run_cta<kF8, kAMN, kBMN, kOut, 2>(a, b, b2, M, N, K, alpha, sa, sb, out, ldo, q, stream);
     return run_cta<kF8, kAMN, kBMN, kOut, 1>(a, b, b2, M, N, K, alpha, sa, sb, out, ldo, q, stream);
 }

@@ -46,3 +46,19 @@ def test_single_cta_gemm_parity():
     tail = (out.stdout + out.stderr)[-3000:]
     assert out.returncode == 0, tail
     assert " passed" in out.stdout and " failed" not in out.stdout, tail
+
+
+@pytest.mark.parametrize("cta,group", [("4", "8"), ("2", "3"), ("2", "0")])
+def test_gemm_cluster_and_raster_parity(cta, group):
+    """COAT_GEMM_CTA=4: two CTA pairs per cluster sharing the B tile by TMA
+    multicast (M > 256; an odd pair-tile count leaves one all-out-of-bounds
+    pair tile, e.g. M = 600).  COAT_GEMM_GROUP_M: the persistent tile walk's
+    raster group -- 3 leaves a ragged last group, 0 is the plain M-fastest
+    walk.  The linear tests (bit-exact epilogues included) pass on each."""
+    env = dict(os.environ, COAT_GEMM_CTA=cta, COAT_GEMM_GROUP_M=group)
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          "tests/test_gpu_linear.py"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    tail = (out.stdout + out.stderr)[-3000:]
+    assert out.returncode == 0, tail
+    assert " passed" in out.stdout and " failed" not in out.stdout, tail
