@@ -45,7 +45,6 @@ constexpr int BM = 128;                   // accumulator rows per CTA (TMEM lane
 constexpr int BN = 256;                   // accumulator columns (MMA N)
 constexpr int BKB = 128;                  // K bytes per stage (one 128B swizzle row)
 constexpr int A_BYTES = BM * BKB;         // 16 KiB
-constexpr int THREADS = 192;
 // Epilogue warps: 4 (one per TMEM lane quarter) -- or 16 for the quantizing
 // gate/up epilogue, whose per-element work (three quantizers + SiLU) is longer
 // than the MMA main loop of a tile with 4 warps (ncu: tensor pipe 62%); each

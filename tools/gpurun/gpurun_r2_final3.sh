@@ -1,0 +1,7 @@
+# full validation after the K4 raster / cluster changes
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/r2
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/r2/t_gpu_final3.log 2>&1; echo "gpu tests rc=$?"
+tail -5 gpurun_out/r2/t_gpu_final3.log
+timeout 600 python bench.py > gpurun_out/r2/bench_default3.json 2>gpurun_out/r2/bench_default3.err; echo "bench rc=$?"; tail -c 600 gpurun_out/r2/bench_default3.json
