@@ -735,27 +735,23 @@ bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t c
     return r == CUDA_SUCCESS;
 }
 
-// Co-resident clusters of 4 (GPC boundaries leave some SMs out), cached per kernel.
+// Co-resident clusters of 4 (GPC boundaries leave some SMs out).
 template <typename K>
 int max_clusters4(K kern, int smem, int threads) {
-    static int cached = -1;
-    if (cached < 0) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(4 * 64);
-        cfg.blockDim = dim3(threads);
-        cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 4;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
-        cached = n;
-    }
-    return cached;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(4 * 64);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    return n;
 }
 
 // COAT_GEMM_GROUP_M overrides the raster group (A/B; 0 or >= tiles_m = the
@@ -812,7 +808,11 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     P.q = q;
     const int ntiles = P.tiles_m * P.tiles_n;
     int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
-    if (kCta == 4) units = max_clusters4(kern, G::SMEM_BYTES + epi_smem_bytes<kOut>(), threads_for<kOut>());
+    if (kCta == 4) {
+        // per kernel instantiation, queried once (thread-safe static initialisation)
+        static const int clusters4 = max_clusters4(kern, G::SMEM_BYTES + epi_smem_bytes<kOut>(), threads_for<kOut>());
+        units = clusters4;
+    }
     if (units <= 0) return cudaErrorInvalidConfiguration;
     const int grid = kCta * (ntiles < units ? ntiles : units);
     if (kCta == 1) {

@@ -172,12 +172,6 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     return v;
 }
 
-struct Workspace {
-    uint32_t* buf = nullptr;
-    size_t words = 0;
-    int dev = -1;
-};
-
 }  // namespace
 
 cudaError_t launch_mgaq_batch(const MgaqItem* items, int n, uint32_t* flags, cudaStream_t st) {
@@ -211,31 +205,40 @@ cudaError_t launch_mgaq_batch(const MgaqItem* items, int n, uint32_t* flags, cud
     P.npt = npt;
     P.flags = flags;
 
-    static Workspace ws;
+    // occupancy per device (queried once); the grid barrier word and the
+    // per-CTA partials are a stream-ordered allocation of this call, so
+    // concurrent batches on different streams never share them
     static std::mutex mu;
+    static int per_sm_of[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    static int per_sm = 0;
+    int per_sm = 0;
     {
         std::lock_guard<std::mutex> lock(mu);
-        if (ws.dev != dev) {
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgaq_batch_kernel, kThreads, 0);
+        if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+        if (per_sm_of[dev] == 0) {
+            const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_of[dev], mgaq_batch_kernel,
+                                                                                kThreads, 0);
             if (e != cudaSuccess) return e;
-            if (ws.buf) cudaFree(ws.buf);
-            ws.words = size_t(kMgaqMaxItems) * device_sm_count() * (per_sm > 0 ? per_sm : 1) + 32;
-            e = cudaMalloc(&ws.buf, ws.words * sizeof(uint32_t));
-            if (e != cudaSuccess) return e;
-            ws.dev = dev;
+            if (per_sm_of[dev] <= 0) per_sm_of[dev] = 1;
         }
+        per_sm = per_sm_of[dev];
     }
-    const int grid = device_sm_count() * (per_sm > 0 ? per_sm : 1);
-    P.barrier = ws.buf;
-    P.partials = ws.buf + 32;
-    cudaError_t e = cudaMemsetAsync(P.barrier, 0, sizeof(uint32_t), st);
+    const int grid = device_sm_count() * per_sm;
+    const size_t words = size_t(kMgaqMaxItems) * size_t(grid) + 32;
+    uint32_t* buf = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), words * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
-    float nz = -0.0f;
-    void* args[] = {&P, &nz};
-    return cudaLaunchCooperativeKernel((void*)mgaq_batch_kernel, dim3(grid), dim3(kThreads), args, 0, st);
+    P.barrier = buf;
+    P.partials = buf + 32;
+    e = cudaMemsetAsync(P.barrier, 0, sizeof(uint32_t), st);
+    if (e == cudaSuccess) {
+        float nz = -0.0f;
+        void* args[] = {&P, &nz};
+        e = cudaLaunchCooperativeKernel((void*)mgaq_batch_kernel, dim3(grid), dim3(kThreads), args, 0, st);
+    }
+    const cudaError_t f = cudaFreeAsync(buf, st);
+    return e != cudaSuccess ? e : f;
 }
 
 // ---------------------------------------------------------------------------
@@ -464,10 +467,12 @@ cudaError_t launch_mgaq_queue(const MgaqItem* items, int n, uint32_t* flags, cud
         if (items[i].dtype != dt || (items[i].group_size != 0 && items[i].group_size != 16))
             return launch_mgaq_streams(items, n, flags, st);   // the kernel's specialisation does not apply
     const int smem = kSlots * kTaskBytes;
+    static std::mutex occ_mu;
     static int per_sm[2] = {0, 0};
     static int occ_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
+    std::unique_lock<std::mutex> occ_lock(occ_mu);
     if (occ_dev != dev) {
         cudaError_t e = cudaFuncSetAttribute(mgaq_queue_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e == cudaSuccess)
@@ -480,6 +485,7 @@ cudaError_t launch_mgaq_queue(const MgaqItem* items, int n, uint32_t* flags, cud
         occ_dev = dev;
     }
     const int grid = device_sm_count() * (per_sm[dt] > 0 ? per_sm[dt] : 1);
+    occ_lock.unlock();
     const int64_t tc = dt == 0 ? task_chunks<0>() : task_chunks<1>();
     QParams P{};
     std::vector<int> pt, pg;

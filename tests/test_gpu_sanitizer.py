@@ -2,9 +2,9 @@
 detection / sanitizers").  racecheck (shared-memory hazards of the mbarrier /
 TMA round pipeline of K1 and the GEMM's staging), synccheck (barrier misuse),
 memcheck (out-of-bounds / misaligned accesses) on small invocations of every
-K1 layout (COAT_K1_EW = 6 / 7 / 8), both forms of coat_quantize_batch, both
-GEMM kernels (CTA pair, single CTA) with and without the quantizing
-epilogues, and the peer-memory ZeRO step on two virtual ranks.  Each report is written to
+K1 layout (COAT_K1_EW = 6 / 7 / 8), both forms of coat_quantize_batch, the
+GEMM kernels (CTA pair, single CTA, two-pair multicast cluster) with and
+without the quantizing epilogues, and the peer-memory ZeRO step on two virtual ranks.  Each report is written to
 gpurun_out/sanitizer/ (summaries committed under profiles/r02/)."""
 import os
 import re
@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 SANITIZER = "/usr/local/cuda/bin/compute-sanitizer"
 CASES = [("k1", {"COAT_K1_EW": "8"}), ("k1", {"COAT_K1_EW": "7"}), ("k1", {"COAT_K1_EW": "6"}),
          ("mgaq", {}), ("mgaq", {"COAT_MGAQ_BATCH": "coop"}), ("mgaq16", {"COAT_MGAQ_BATCH": "queue"}),
-         ("gemm", {}), ("gemm", {"COAT_GEMM_CTA": "1"}), ("epi", {}), ("epi", {"COAT_GEMM_CTA": "1"}),
+         ("gemm", {}), ("gemm", {"COAT_GEMM_CTA": "1"}), ("gemm", {"COAT_GEMM_CTA": "4"}), ("epi", {}), ("epi", {"COAT_GEMM_CTA": "1"}),
          ("p2p", {})]
 
 
@@ -65,8 +65,8 @@ def test_compute_sanitizer_clean(sanitizer_runs, tool, which, env):
     rc, stdout, stderr, report = sanitizer_runs[_tag(tool, which, env)]
     assert f"sanitize workload {which} ok" in stdout, (stdout[-1000:], stderr[-2000:])
     hazards = [h for h in re.split(r"\n(?==+ Error: )", report) if "Error: " in h]
-    if tool == "racecheck" and which in ("gemm", "epi") and not env:
-        # The CTA-pair kernel's only reports are "(CUDA barrier operation)"
+    if tool == "racecheck" and which in ("gemm", "epi") and env.get("COAT_GEMM_CTA", "2") != "1":
+        # The CTA-pair (and two-pair cluster) kernel's only reports are "(CUDA barrier operation)"
         # hazards inside the first 1 KB of shared memory -- the window the
         # hardware reserves for itself on sm_90+ (cluster barrier / paired
         # TMEM allocator), written by no instruction of the kernel (negative

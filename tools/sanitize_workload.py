@@ -9,7 +9,8 @@ family, for `compute-sanitizer --tool racecheck|synccheck|memcheck`
   mgaq16 coat_quantize_batch over bf16 per-group 1x16 and per-tensor records
          (the shape the COAT_MGAQ_BATCH=queue task-queue kernel takes)
   gemm   the FP8 forward and the BF16 dgrad / wgrad (COAT_GEMM_CTA=1: the
-         single-CTA kernel; default the CTA-pair kernel)
+         single-CTA kernel, =4 the two-pair multicast cluster; default the
+         CTA-pair kernel)
   epi    the quantizing GEMM epilogues: per-group 1x16 output and the fused
          gate/up + SiLU*mul block (+ its down.in pass)
   p2p    coat_zero_step_p2p on 2 virtual ranks (peer-load reduce-scatter, K1,
@@ -56,7 +57,7 @@ def main(which):
         torch.cuda.synchronize()
         assert len(qs) == len(xs)
     elif which == "gemm":
-        M, K, N = 256, 512, 384
+        M, K, N = 608, 512, 384   # 3 pair tiles: COAT_GEMM_CTA=4 leaves one all-out-of-bounds pair tile
         x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         w = torch.randn(K, N, device="cuda") / K ** 0.5
         qx = coat.quantize(x, coat.QuantGeometry.per_tensor())
