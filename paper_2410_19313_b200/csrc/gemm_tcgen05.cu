@@ -63,9 +63,20 @@ __host__ __device__ constexpr int threads_for() { return 64 + 32 * epi_warps<kOu
 #ifndef COAT_GEMM_COALESCED
 #define COAT_GEMM_COALESCED 1
 #endif
+// fp32 epilogue by TMA bulk-tensor stores from a swizzled 32 x 32 staging
+// tile per warp (double-buffered) instead of STG
+#ifndef COAT_GEMM_TMA_STORE
+#define COAT_GEMM_TMA_STORE 1
+#endif
+template <int kOut>
+__host__ __device__ constexpr bool tma_store() {
+    return kOut == 0 && COAT_GEMM_TMA_STORE;
+}
 template <int kOut>
 __host__ __device__ constexpr int epi_smem_bytes() {
-    return (kOut == 0 && COAT_GEMM_COALESCED) ? epi_warps<kOut>() * 32 * 36 * 4 : 0;
+    // TMA store: the staging tiles start at the next 1 KB boundary after the barriers
+    return tma_store<kOut>() ? 768 + epi_warps<kOut>() * 2 * 4096
+                             : (kOut == 0 && COAT_GEMM_COALESCED) ? epi_warps<kOut>() * 32 * 36 * 4 : 0;
 }
 constexpr int ACC_COLS = BN;              // fp32 columns per accumulator
 constexpr int TMEM_COLS = 2 * ACC_COLS;   // double buffer = all 512 columns
@@ -125,6 +136,7 @@ struct Params {
     const uint16_t* scale_b;
     void* out;
     int64_t ldo;               // elements
+    int tma_out;               // kOutF32 with tma_store(): map_b2 is the output's tensor map
     EpiQ q;
 };
 
@@ -193,6 +205,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
             smem_u32(dst)),
         "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
+}
+// one lane of the (converged) warp -- the lowest, so always the same one
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+    return p != 0;
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -316,6 +334,28 @@ __device__ __forceinline__ uint32_t quant16_store(const aq::Chunk16& y, uint8_t*
         *scale = float_to_bf16_bits_exact(s);
     }
     return f2u(m) >= 0x7F800000u ? 1u : 0u;
+}
+
+// fp32 output row segment store.  COAT_GEMM_STORE_HINT: 0 plain, 1 streaming
+// (.cs), 2 L2 evict_first policy -- the output is written once and never
+// re-read by the kernel, so it should not displace the A / B operands in L2.
+#ifndef COAT_GEMM_STORE_HINT
+#define COAT_GEMM_STORE_HINT 0
+#endif
+__device__ __forceinline__ void st_out4(float* p, const float4& v, uint64_t policy) {
+#if defined(COAT_GEMM_DIAG_NOSTG)
+    if (v.x == 1.2345e-38f) *reinterpret_cast<float4*>(p) = v;   // measurement only: (almost) no stores
+#elif COAT_GEMM_STORE_HINT == 1
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+#elif COAT_GEMM_STORE_HINT == 2
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(policy)
+                 : "memory");
+#else
+    (void)policy;
+    *reinterpret_cast<float4*>(p) = v;
+#endif
 }
 
 template <bool kF8, bool kAMN, bool kBMN, int kOut, int kCta>
@@ -474,13 +514,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer (pair: leader only)
-        if (lane == 0 && rank == 0) {
+        // The whole warp runs the loop (warp-uniform control flow, so the
+        // descriptors live in uniform registers); one elected lane -- always
+        // the same, lane 0 -- issues the MMAs and their commits.  A single-lane
+        // loop made the compiler wrap every tcgen05.mma in an elect / R2UR
+        // broadcast sequence (~23 SASS instructions per MMA), slow enough that
+        // the epilogue warp sharing the scheduler pushed it past the MMA time.
+        if (rank == 0) {
             constexpr uint32_t idesc = instr_desc(kF8, kAMN, kBMN, G::TILE_M);
             // per-MMA K advance inside a stage (bytes): K-major +32 B, MN-major +UK rows of 128 B
             constexpr uint32_t a_step = kAMN ? UK * 128 : 32;
             constexpr uint32_t b_step = kBMN ? UK * 128 : 32;
             constexpr uint32_t a_lbo = kAMN ? BK * 128 : 16;
             constexpr uint32_t b_lbo = kBMN ? BK * 128 : 16;
+            // stage-0 descriptors; a stage / K step only adds to the address field
+            // (bits 0-13 = address >> 4; every smem address < 256 KB, so no carry)
+            const uint64_t adesc0 = smem_desc(smem_u32(smem), a_lbo, 1024);
+            const uint64_t bdesc0 = smem_desc(smem_u32(smem) + A_BYTES, b_lbo, 1024);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -492,25 +542,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 for (int kb = 0; kb < P.k_blocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-                    const uint32_t sb = sa + A_BYTES;
+                    const uint64_t so = uint64_t(uint32_t(stage * STAGE_BYTES) >> 4);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < BK / UK; ++kk) {
-                        const uint64_t ad = smem_desc(sa + kk * a_step, a_lbo, 1024);
-                        const uint64_t bd = smem_desc(sb + kk * b_step, b_lbo, 1024);
-                        tc_mma<kF8, kCta>(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        for (int kk = 0; kk < BK / UK; ++kk)
+                            tc_mma<kF8, kCta>(tmem_d, adesc0 + so + uint64_t((kk * a_step) >> 4),
+                                              bdesc0 + so + uint64_t((kk * b_step) >> 4), idesc,
+                                              (kb | kk) != 0 ? 1u : 0u);
+                        // frees the smem stage (in both CTAs) when these MMAs retire
+                        if (kCta == 1) tc_commit(&empty[stage]);
+                        else tc_commit_pair(&empty[stage], kCta == 4 ? uint16_t(0xF) : uint16_t(3));
                     }
-                    // frees the smem stage (in both CTAs) when these MMAs retire
-                    if (kCta == 1) tc_commit(&empty[stage]);
-                    else tc_commit_pair(&empty[stage], kCta == 4 ? uint16_t(0xF) : uint16_t(3));
+                    __syncwarp();
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
+
                 // accumulator ready for the epilogue(s)
-                if (kCta == 1) tc_commit(&tfull[acc]);
-                else tc_commit_pair(&tfull[acc], uint16_t(3u << (2 * pidx)));
+                if (elect_one()) {
+                    if (kCta == 1) tc_commit(&tfull[acc]);
+                    else tc_commit_pair(&tfull[acc], uint16_t(3u << (2 * pidx)));
+                }
+                __syncwarp();
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1u;
@@ -524,12 +579,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         const int row_in_tile = int(rank) * BM + q * 32 + lane;
         // kOutF32: this warp's 32 x 36-float staging tile behind the barriers
         const uint32_t stile = smem_u32(smem + STAGES * STAGE_BYTES + 256) + uint32_t((warp - 2) * (32 * 36) * 4);
+        // tma_store(): this warp's two 4 KB swizzled staging tiles (1 KB aligned)
+        const uint32_t ttile = smem_u32(smem + STAGES * STAGE_BYTES + 1024) + uint32_t((warp - 2) * 8192);
+        uint32_t tbuf = 0;
         const uint32_t tempty_leader0 = kCta >= 2 ? cluster_addr(&tempty[0], crank & ~1u) : 0u;
         float alpha = P.alpha;
         if (P.scale_a) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_a));
         float alpha_u = alpha;
         if (P.scale_b) alpha = __fmul_rn(alpha, bf16_bits_to_float(*P.scale_b));
         if (kOut == kOutUpGate && P.q.scale_b1) alpha_u = __fmul_rn(alpha_u, bf16_bits_to_float(*P.q.scale_b1));
+        uint64_t out_policy;
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(out_policy));
         uint32_t bad = 0;
         float amp = 0.0f;   // kOutUpGate: max |product| (max.f32: NaN ignored, Inf kept)
         int acc = 0;
@@ -598,6 +658,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 tmem_ld32(taddr + uint32_t(c * 32), r);
                 tmem_wait_ld();
                 const int col0 = nb * BN + c * 32;
+#ifdef COAT_GEMM_DIAG_NOEPI
+                // measurement only (wrong results): TMEM drained, nothing stored
+                if (r[0] == 0x7fc00001u) bad |= 1u;
+                continue;
+#endif
                 if (kOut == kOutQ16) {
                     const bool live = row < P.M;
                     const int64_t rq = live ? row : 0;
@@ -616,6 +681,32 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                         }
                         bad |= quant16_store(y, P.q.c0 + rq * P.q.ldc + col, P.q.s0 + rq * (P.q.ldc >> 4) + (col >> 4),
                                              -0.0f, live) & (live ? 1u : 0u);
+                    }
+                } else if (tma_store<kOut>() && P.tma_out) {
+                    // rows / columns outside the output are clipped by the TMA unit
+                    if (col0 < P.N && row_base < P.M) {
+                        const uint32_t buf = ttile + (tbuf & 1u) * 4096u;
+                        // the store issued from this buffer two chunks ago has read it
+                        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)   // 16-byte chunk i of this lane's row, 128B-swizzled
+                            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                             buf + uint32_t(lane * 128 + ((i ^ (lane & 7)) << 4))),
+                                         "f"(__fmul_rn(alpha, u2f(r[4 * i]))), "f"(__fmul_rn(alpha, u2f(r[4 * i + 1]))),
+                                         "f"(__fmul_rn(alpha, u2f(r[4 * i + 2]))), "f"(__fmul_rn(alpha, u2f(r[4 * i + 3])))
+                                         : "memory");
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                    &map_b2),
+                                "r"(col0), "r"(row_base), "r"(buf)
+                                : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                        ++tbuf;
                     }
                 } else if (kOut == kOutF32 && COAT_GEMM_COALESCED && col0 + 32 <= P.N && row_base + 32 <= P.M) {
                     // the warp's 32 rows x 32 columns through a padded shared-memory
@@ -638,7 +729,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                                      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                                      : "r"(stile + uint32_t((rr * 36 + cc) * 4))
                                      : "memory");
-                        *reinterpret_cast<float4*>(o + int64_t(rr) * P.ldo + cc) = v;
+                        st_out4(o + int64_t(rr) * P.ldo + cc, v, out_policy);
                     }
                     __syncwarp();
                 } else if (row < P.M) {
@@ -692,6 +783,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         if (kOut >= kOutQ16 && P.q.flags && __reduce_or_sync(0xFFFFFFFFu, bad) && lane == 0)
             atomicOr(P.q.flags, kFlagNonFiniteInput);
+        if (tma_store<kOut>() && P.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     if (kCta >= 2) cluster_sync_all();   // no CTA of the cluster leaves while another may still signal it
@@ -721,14 +813,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D tensor map over a row-major matrix [rows][cols] of `esz`-byte elements,
 // box = (box_cols, box_rows), 128B swizzle, zero fill out of bounds.
-bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t cols, int box_cols, int box_rows,
+              int64_t ld = 0) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-    const cuuint64_t strides[1] = {cuuint64_t(cols) * cuuint64_t(esz)};
+    const cuuint64_t strides[1] = {cuuint64_t(ld ? ld : cols) * cuuint64_t(esz)};
     const cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = fn(m, esz == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+    const CUtensorMapDataType dt = esz == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUresult r = fn(m, dt, 2,
                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -781,6 +877,11 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     const bool ok_b2 = kOut == kOutUpGate ? make_map(&mb2, b2, ESZ, K, N, 128 / ESZ, BK) : true;
     if (!ok_a || !ok_b || !ok_b2) return cudaErrorInvalidValue;
     if (kOut != kOutUpGate) mb2 = mb;
+    // tma_store(): the output [M, N] fp32 with row pitch ldo as 32 x 32 boxes (needs a 16-byte pitch)
+    int tma_out = 0;
+    if (tma_store<kOut>() && (ldo * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0 &&
+        make_map(&mb2, out, 4, M, N, 32, 32, ldo))
+        tma_out = 1;
     auto kern = gemm_kernel<kF8, kAMN, kBMN, kOut, kCta>;
     static int attr_dev = -1;
     int dev = 0;
@@ -805,6 +906,7 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     P.scale_b = sb;
     P.out = out;
     P.ldo = ldo;
+    P.tma_out = tma_out;
     P.q = q;
     const int ntiles = P.tiles_m * P.tiles_n;
     int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
