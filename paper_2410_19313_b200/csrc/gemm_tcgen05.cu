@@ -702,7 +702,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                             asm volatile(
                                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                     &map_b2),
+#ifdef COAT_GEMM_DIAG_ALIAS
+                                "r"(col0), "r"(row_base & 255), "r"(buf)   // measurement only: 256 output rows reused
+#else
                                 "r"(col0), "r"(row_base), "r"(buf)
+#endif
                                 : "memory");
                             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                         }
