@@ -137,6 +137,7 @@ struct Params {
     void* out;
     int64_t ldo;               // elements
     int tma_out;               // kOutF32 with tma_store(): map_b2 is the output's tensor map
+    unsigned epi_pause_ns;     // pause between a warp's epilogue chunks (see epi_pause_ns())
     EpiQ q;
 };
 
@@ -654,6 +655,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 #pragma unroll 1
             for (int c = half * (BN / 32) * 4 / epi_warps<kOut>(); c < (half + 1) * (BN / 32) * 4 / epi_warps<kOut>();
                  ++c) {
+                // spread the tile's output writes: a pause before every chunk but the first
+                if (P.epi_pause_ns && c != half * (BN / 32) * 4 / epi_warps<kOut>()) __nanosleep(P.epi_pause_ns);
                 uint32_t r[32];
                 tmem_ld32(taddr + uint32_t(c * 32), r);
                 tmem_wait_ld();
@@ -854,6 +857,26 @@ int max_clusters4(K kern, int smem, int threads) {
     return n;
 }
 
+// Epilogue write spreading.  The CTAs finish their tiles in lock step, and the
+// output writes of a whole tile leaving every SM at once compete with the next
+// tile's operand loads (ncu: FP8 forward tensor pipe 88% with its fp32 output
+// stores, 97% without; the SM -> L2 write traffic, not the DRAM write-back).
+// A pause between a warp's 32-column chunks spreads the writes over the next
+// main loop: k_blocks * COAT_GEMM_EPI_PAUSE_PER_KB ns for the fp32 outputs
+// (default 20: 800 ns per chunk on the cfg4 forward; 7 pauses are ~1/3 of a
+// main loop of ~512 cycles per k-block at the power-capped ~1.3 GHz, so the
+// epilogue still finishes before its accumulator is needed).  ncu, cfg4
+// forward: 399 -> 382 us, tensor pipe 88 -> 95%.  Not for the bf16 dgrad
+// output (64 KB per tile over a long K loop: pausing measured -3%).
+inline unsigned epi_pause_ns(int k_blocks) {
+    static const int per_kb = [] {
+        const char* e = getenv("COAT_GEMM_EPI_PAUSE_PER_KB");
+        return e ? atoi(e) : 20;
+    }();
+    const long v = long(per_kb) * long(k_blocks);
+    return unsigned(v < 0 ? 0 : v > 8000 ? 8000 : v);
+}
+
 // COAT_GEMM_GROUP_M overrides the raster group (A/B; 0 or >= tiles_m = the
 // plain M-fastest walk).
 inline int raster_group_m(int tiles_m) {
@@ -911,6 +934,7 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     P.out = out;
     P.ldo = ldo;
     P.tma_out = tma_out;
+    P.epi_pause_ns = kOut == kOutF32 ? epi_pause_ns(P.k_blocks) : 0u;   // the 4-byte outputs only
     P.q = q;
     const int ntiles = P.tiles_m * P.tiles_n;
     int units = device_sm_count() / kCta;   // persistent: one CTA (pair) per SM (TPC)
