@@ -15,9 +15,14 @@
 // Persistent, warp-specialized, TMA (SWIZZLE_128B) -> smem ring of 128-byte K
 // slices:
 //   warp 0: TMA producer (one elected lane)       full/empty mbarriers per stage
-//   warp 1: TMEM allocator + MMA issuer (one lane) tcgen05.mma + tcgen05.commit
-//   warps 2-5: epilogue (TMEM lanes 0-127)        double-buffered accumulator
-// Two variants (kCta):
+//   warp 1: TMEM allocator + MMA issuer (the warp  tcgen05.mma + tcgen05.commit
+//           runs the loop, elect.sync issues)
+//   warps 2-5 (2-17 for the gate/up epilogue):    double-buffered accumulator
+//           epilogue, tcgen05.ld -> fp32 output by TMA bulk-tensor stores from
+//           swizzled staging tiles (writes spread over the next main loop), or
+//           bf16 / per-group 1x16 codes / the gate/up SiLU*mul quantizers
+// Tiles are walked in groups of 8 M blocks (the CTAs in flight share operands
+// in L2).  Variants (kCta):
 //   1: one CTA per SM, 128 x 256 tile, cta_group::1 (small M).
 //   2: a CTA pair on the two SMs of a TPC (cluster of 2), 256 x 256 tile,
 //      tcgen05.mma.cta_group::2 issued by the leader.  Each CTA stages only its
@@ -27,6 +32,8 @@
 //      tensor pipe.  Both CTAs' TMA bytes land on the leader's full barrier
 //      (.cta_group::2 TMA, mapa address); commits multicast to both CTAs; both
 //      CTAs' epilogues arrive on the leader's TMEM-empty barrier.
+//   4: two CTA pairs per cluster sharing B by TMA multicast (COAT_GEMM_CTA=4;
+//      parity-tested, measured slower -- DESIGN.md K4).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
