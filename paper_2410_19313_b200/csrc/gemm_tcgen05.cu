@@ -38,6 +38,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
 
@@ -79,11 +80,17 @@ template <int kOut>
 __host__ __device__ constexpr bool tma_store() {
     return kOut == 0 && COAT_GEMM_TMA_STORE;
 }
+// Gate/up epilogue staging (see the kernel): per TMEM lane quarter and output
+// array (silu.in, mul.in.silu, mul.in.up) a 32-row x 128-byte code tile
+// (128B-swizzled, 1 KB aligned) and a 32-row x 16-byte scale tile.
+constexpr int kUgCodeTile = 32 * 128, kUgScaleTile = 32 * 16;
+constexpr int kUgStageBytes = 12 * kUgCodeTile + 12 * kUgScaleTile;
 template <int kOut>
 __host__ __device__ constexpr int epi_smem_bytes() {
     // TMA store: the staging tiles start at the next 1 KB boundary after the barriers
     return tma_store<kOut>() ? 768 + epi_warps<kOut>() * 2 * 4096
-                             : (kOut == 0 && COAT_GEMM_COALESCED) ? epi_warps<kOut>() * 32 * 36 * 4 : 0;
+           : kOut == 3       ? 768 + kUgStageBytes
+           : (kOut == 0 && COAT_GEMM_COALESCED) ? epi_warps<kOut>() * 32 * 36 * 4 : 0;
 }
 constexpr int ACC_COLS = BN;              // fp32 columns per accumulator
 constexpr int TMEM_COLS = 2 * ACC_COLS;   // double buffer = all 512 columns
@@ -92,7 +99,7 @@ constexpr int TMEM_COLS = 2 * ACC_COLS;   // double buffer = all 512 columns
 // share the B tile (same N block, adjacent M blocks): each CTA loads half of
 // its B half and multicasts it to the same-rank CTA of the other pair, so the
 // L2 -> SM operand traffic per FLOP drops by another quarter.
-template <int kCta>
+template <int kCta, int kOut = 0>
 struct Geo {
     static constexpr int PAIR = kCta >= 2 ? 2 : 1;         // CTAs per MMA
     static constexpr int BN_L = BN / PAIR;                 // B rows staged by this CTA
@@ -101,7 +108,8 @@ struct Geo {
 #ifndef COAT_GEMM_PAIR_STAGES
 #define COAT_GEMM_PAIR_STAGES 6
 #endif
-    static constexpr int STAGES = kCta >= 2 ? COAT_GEMM_PAIR_STAGES : 4;
+    // the gate/up kernel gives one stage to its epilogue staging tiles
+    static constexpr int STAGES = kCta >= 2 ? (kOut == 3 ? 5 : COAT_GEMM_PAIR_STAGES) : (kOut == 3 ? 3 : 4);
     static constexpr int TILE_M = BM * PAIR;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -134,6 +142,14 @@ struct EpiQ {
     int64_t ldc;
 };
 
+// kOutUpGate with P.ug_tma: TMA store maps of the three code arrays (uint8
+// [M, ldc], 128 x 32 boxes, 128B swizzle) and their scale arrays (bf16
+// [M, ldc / 16], 8 x 32 boxes)
+struct EpiMaps {
+    CUtensorMap c[3];
+    CUtensorMap s[3];
+};
+
 struct Params {
     int M, N, K;               // K in elements
     int tiles_m, tiles_n, k_blocks;
@@ -144,6 +160,7 @@ struct Params {
     void* out;
     int64_t ldo;               // elements
     int tma_out;               // kOutF32 with tma_store(): map_b2 is the output's tensor map
+    int ug_tma;                // kOutUpGate: codes and scales through the staging tiles + emaps
     unsigned epi_pause_ns;     // pause between a warp's epilogue chunks (see epi_pause_ns())
     EpiQ q;
 };
@@ -369,9 +386,9 @@ __device__ __forceinline__ void st_out4(float* p, const float4& v, uint64_t poli
 template <bool kF8, bool kAMN, bool kBMN, int kOut, int kCta>
 __global__ void __launch_bounds__(threads_for<kOut>(), 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-            const __grid_constant__ CUtensorMap map_b2, Params P) {
+            const __grid_constant__ CUtensorMap map_b2, const __grid_constant__ EpiMaps emaps, Params P) {
     static_assert(kOut != kOutUpGate || (kF8 && kBMN), "gate/up epilogue: FP8 forward, W (K, N) row-major");
-    using G = Geo<kCta>;
+    using G = Geo<kCta, kOut>;
     constexpr int STAGES = G::STAGES;
     constexpr int STAGE_BYTES = G::STAGE_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -616,6 +633,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 const bool live = row < P.M;
                 const int64_t rq = live ? row : 0;
                 constexpr int kGroups = 8 * 4 / epi_warps<kOut>();   // 16-column groups per warp (of 8 per half)
+                // P.ug_tma: the four warps of this TMEM lane quarter put their codes and
+                // scales into the quarter's staging tiles, and one of them writes each
+                // tile to HBM with a TMA store (32 rows x 128 B of codes per array, whole
+                // row segments) instead of 32 scattered 16-byte and 2-byte stores per
+                // warp instruction (the scattered stores cost the kernel ~14%: ncu, with
+                // them removed, 727 vs 843 us, tensor pipe 98 vs 86%)
+                const uint32_t ug_code = smem_u32(smem + STAGES * STAGE_BYTES + 1024) + uint32_t(q * 3 * kUgCodeTile);
+                const uint32_t ug_scale = smem_u32(smem + STAGES * STAGE_BYTES + 1024) + uint32_t(12 * kUgCodeTile) +
+                                          uint32_t(q * 3 * kUgScaleTile);
+                const bool ug_issuer = half == 0 && lane == 0;
+                auto ug_put = [&](int a, int gi, const uint4& cw, uint16_t sbits) {
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                     ug_code + uint32_t(a * kUgCodeTile + lane * 128 + ((gi ^ (lane & 7)) << 4))),
+                                 "r"(cw.x), "r"(cw.y), "r"(cw.z), "r"(cw.w)
+                                 : "memory");
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(ug_scale + uint32_t(a * kUgScaleTile + lane * 16 + gi * 2)),
+                                 "h"(sbits)
+                                 : "memory");
+                };
+                if (P.ug_tma) {
+                    // the previous tile's stores have read the staging tiles
+                    if (ug_issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+                }
 #pragma unroll 1
                 for (int gi = half * kGroups; gi < (half + 1) * kGroups; ++gi) {
                     uint32_t rg[16], ru[16];
@@ -644,18 +685,42 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                     uint16_t sbits;
                     float gam;
                     bad |= aq::quant_dq16(gv, cw, sbits, -0.0f, &gam);   // silu.in
-                    if (live) { *reinterpret_cast<uint4*>(P.q.c0 + co) = cw; P.q.s0[so] = sbits; }
+                    if (P.ug_tma) ug_put(0, gi, cw, sbits);
+                    else if (live) { *reinterpret_cast<uint4*>(P.q.c0 + co) = cw; P.q.s0[so] = sbits; }
                     aq::silu16(gv, -0.0f, gam);
                     bad |= aq::quant_dq16(gv, cw, sbits, -0.0f);   // mul.in.silu
-                    if (live) { *reinterpret_cast<uint4*>(P.q.c1 + co) = cw; P.q.s1[so] = sbits; }
+                    if (P.ug_tma) ug_put(1, gi, cw, sbits);
+                    else if (live) { *reinterpret_cast<uint4*>(P.q.c1 + co) = cw; P.q.s1[so] = sbits; }
                     bad |= aq::quant_dq16(uv, cw, sbits, -0.0f);   // mul.in.up
-                    if (live) { *reinterpret_cast<uint4*>(P.q.c2 + co) = cw; P.q.s2[so] = sbits; }
+                    if (P.ug_tma) ug_put(2, gi, cw, sbits);
+                    else if (live) { *reinterpret_cast<uint4*>(P.q.c2 + co) = cw; P.q.s2[so] = sbits; }
                     if (live) {
 #pragma unroll
                         for (int i = 0; i < 16; i += 2) {
                             const F2 pr = f2_mul(F2{gv.v[i], gv.v[i + 1]}, F2{uv.v[i], uv.v[i + 1]}, -0.0f);
                             asm("max.f32 %0, %1, %2, %3;" : "=f"(amp) : "f"(amp), "f"(fabsf(pr.x)), "f"(fabsf(pr.y)));
                         }
+                    }
+                }
+                if (P.ug_tma) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+                    if (ug_issuer) {
+                        // rows >= M and columns >= N are clipped by the TMA unit
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                    &emaps.c[a]),
+                                "r"(nb * 128), "r"(row_base), "r"(ug_code + uint32_t(a * kUgCodeTile))
+                                : "memory");
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                    &emaps.s[a]),
+                                "r"(nb * 8), "r"(row_base), "r"(ug_scale + uint32_t(a * kUgScaleTile))
+                                : "memory");
+                        }
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
                 }
             } else
@@ -798,6 +863,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (kOut >= kOutQ16 && P.q.flags && __reduce_or_sync(0xFFFFFFFFu, bad) && lane == 0)
             atomicOr(P.q.flags, kFlagNonFiniteInput);
         if (tma_store<kOut>() && P.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (kOut == kOutUpGate && P.ug_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     if (kCta >= 2) cluster_sync_all();   // no CTA of the cluster leaves while another may still signal it
@@ -828,7 +894,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 2-D tensor map over a row-major matrix [rows][cols] of `esz`-byte elements,
 // box = (box_cols, box_rows), 128B swizzle, zero fill out of bounds.
 bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t cols, int box_cols, int box_rows,
-              int64_t ld = 0) {
+              int64_t ld = 0, bool swizzle = true) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
@@ -840,7 +906,8 @@ bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t c
                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUresult r = fn(m, dt, 2,
                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -898,10 +965,24 @@ template <bool kF8, bool kAMN, bool kBMN, int kOut, int kCta>
 cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, int K, float alpha,
                     const uint16_t* sa, const uint16_t* sb, void* out, int64_t ldo, const EpiQ& q,
                     cudaStream_t stream) {
-    using G = Geo<kCta>;
+    using G = Geo<kCta, kOut>;
     constexpr int ESZ = kF8 ? 1 : 2;
     constexpr int BK = BKB / ESZ;
     CUtensorMap ma, mb, mb2;
+    EpiMaps em;
+    memset(&em, 0, sizeof(em));
+    // kOutUpGate: the codes (uint8 [M, ldc]) and scales (bf16 [M, ldc/16]) as TMA store
+    // targets; the scale rows need a 16-byte pitch (ldc % 128 == 0), else direct stores
+    int ug_tma = 0;
+    if (kOut == kOutUpGate && (q.ldc % 128) == 0) {
+        uint8_t* cs[3] = {q.c0, q.c1, q.c2};
+        uint16_t* ss[3] = {q.s0, q.s1, q.s2};
+        bool ok = true;
+        for (int a = 0; a < 3 && ok; ++a)
+            ok = make_map(&em.c[a], cs[a], 1, M, N, 128, 32, q.ldc) &&
+                 make_map(&em.s[a], ss[a], 2, M, N / 16, 8, 32, q.ldc / 16, false);
+        ug_tma = ok ? 1 : 0;
+    }
     // A logical [M x K]: K-major memory [M][K]; MN-major memory [K][M]
     const bool ok_a = !kAMN ? make_map(&ma, a, ESZ, M, K, BK, BM) : make_map(&ma, a, ESZ, K, M, 128 / ESZ, BK);
     // kCta 4: the B box is a quarter (half of this CTA's half; see the producer)
@@ -941,6 +1022,7 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     P.out = out;
     P.ldo = ldo;
     P.tma_out = tma_out;
+    P.ug_tma = ug_tma;
     P.epi_pause_ns = kOut == kOutF32 ? epi_pause_ns(P.k_blocks) : 0u;   // the 4-byte outputs only
     P.q = q;
     const int ntiles = P.tiles_m * P.tiles_n;
@@ -953,7 +1035,7 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     if (units <= 0) return cudaErrorInvalidConfiguration;
     const int grid = kCta * (ntiles < units ? ntiles : units);
     if (kCta == 1) {
-        kern<<<grid, threads_for<kOut>(), G::SMEM_BYTES + epi_smem_bytes<kOut>(), stream>>>(ma, mb, mb2, P);
+        kern<<<grid, threads_for<kOut>(), G::SMEM_BYTES + epi_smem_bytes<kOut>(), stream>>>(ma, mb, mb2, em, P);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -968,7 +1050,7 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, ma, mb, mb2, P);
+    return cudaLaunchKernelEx(&cfg, kern, ma, mb, mb2, em, P);
 }
 
 // COAT_GEMM_CTA=1 forces the single-CTA kernel, =4 the two-pair B-multicast

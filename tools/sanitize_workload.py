@@ -76,8 +76,15 @@ def main(which):
         qu = coat.quantize(torch.randn(K, N, device="cuda") / K ** 0.5, coat.QuantGeometry.per_tensor())
         q16 = coat.fp8_linear_q16(qx, qg)
         recs = coat.fp8_upgate_silu(qx, qg, qu)
+        # N % 128 == 0: the gate/up codes and scales go through the staging tiles and
+        # TMA stores; 300 rows: a ragged last tile the TMA unit clips
+        M2, N2 = 300, 384
+        qx2 = coat.quantize(torch.randn(M2, K, device="cuda").to(torch.bfloat16), coat.QuantGeometry.per_tensor())
+        qg2 = coat.quantize(torch.randn(K, N2, device="cuda") / K ** 0.5, coat.QuantGeometry.per_tensor())
+        qu2 = coat.quantize(torch.randn(K, N2, device="cuda") / K ** 0.5, coat.QuantGeometry.per_tensor())
+        recs2 = coat.fp8_upgate_silu(qx2, qg2, qu2)
         torch.cuda.synchronize()
-        assert q16.codes.shape == (M, N) and len(recs) == 4
+        assert q16.codes.shape == (M, N) and len(recs) == 4 and len(recs2) == 4
     elif which == "p2p":
         import ctypes as C
         from paper_2410_19313_b200 import _lib
