@@ -85,11 +85,15 @@ __host__ __device__ constexpr bool tma_store() {
 // (128B-swizzled, 1 KB aligned) and a 32-row x 16-byte scale tile.
 constexpr int kUgCodeTile = 32 * 128, kUgScaleTile = 32 * 16;
 constexpr int kUgStageBytes = 12 * kUgCodeTile + 12 * kUgScaleTile;
+// 1x16 epilogue staging per warp: its 32 rows x 256 codes as two 128B-swizzled
+// 32 x 128-byte tiles, and 32 rows x 16 scales (32 bytes)
+constexpr int kQ16StageBytes = 2 * kUgCodeTile + 32 * 32;
 template <int kOut>
 __host__ __device__ constexpr int epi_smem_bytes() {
     // TMA store: the staging tiles start at the next 1 KB boundary after the barriers
     return tma_store<kOut>() ? 768 + epi_warps<kOut>() * 2 * 4096
            : kOut == 3       ? 768 + kUgStageBytes
+           : kOut == 2       ? 768 + epi_warps<kOut>() * kQ16StageBytes
            : (kOut == 0 && COAT_GEMM_COALESCED) ? epi_warps<kOut>() * 32 * 36 * 4 : 0;
 }
 constexpr int ACC_COLS = BN;              // fp32 columns per accumulator
@@ -109,7 +113,8 @@ struct Geo {
 #define COAT_GEMM_PAIR_STAGES 6
 #endif
     // the gate/up kernel gives one stage to its epilogue staging tiles
-    static constexpr int STAGES = kCta >= 2 ? (kOut == 3 ? 5 : COAT_GEMM_PAIR_STAGES) : (kOut == 3 ? 3 : 4);
+    static constexpr int STAGES =
+        kCta >= 2 ? ((kOut == 3 || kOut == 2) ? 5 : COAT_GEMM_PAIR_STAGES) : ((kOut == 3 || kOut == 2) ? 3 : 4);
     static constexpr int TILE_M = BM * PAIR;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -160,7 +165,7 @@ struct Params {
     void* out;
     int64_t ldo;               // elements
     int tma_out;               // kOutF32 with tma_store(): map_b2 is the output's tensor map
-    int ug_tma;                // kOutUpGate: codes and scales through the staging tiles + emaps
+    int ug_tma;                // kOutUpGate / kOutQ16: codes and scales through the staging tiles + emaps
     unsigned epi_pause_ns;     // pause between a warp's epilogue chunks (see epi_pause_ns())
     EpiQ q;
 };
@@ -345,19 +350,15 @@ __host__ __device__ constexpr uint32_t instr_desc(bool f8, bool a_mn, bool b_mn,
 
 // Per-group (1x16) quantization of one 16-column group of y held by this
 // thread (quantize.cpp:89-111 with G = 16: NaN/Inf -> non-finite flag).
-__device__ __forceinline__ uint32_t quant16_store(const aq::Chunk16& y, uint8_t* codes, uint16_t* scale, float nz,
-                                                  bool store) {
+__device__ __forceinline__ uint32_t quant16(const aq::Chunk16& y, uint4& cw, uint16_t& sbits, float nz) {
     float m = aq::fmax3_nan_(fabsf(y.v[0]), fabsf(y.v[1]), fabsf(y.v[2]));
 #pragma unroll
     for (int i = 3; i < 15; i += 2) m = aq::fmax3_nan_(m, fabsf(y.v[i]), fabsf(y.v[i + 1]));
     m = aq::fmax3_nan_(m, fabsf(y.v[15]), 0.0f);
     float s, rs;
     aq::group_scale_fast(f2u(m), s, rs);
-    const uint4 cw = aq::encode16(y, s, rs, nz);
-    if (store) {
-        *reinterpret_cast<uint4*>(codes) = cw;
-        *scale = float_to_bf16_bits_exact(s);
-    }
+    cw = aq::encode16(y, s, rs, nz);
+    sbits = float_to_bf16_bits_exact(s);
     return f2u(m) >= 0x7F800000u ? 1u : 0u;
 }
 
@@ -723,7 +724,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
                 }
-            } else
+            } else {
+            // kOutQ16 with P.ug_tma: this warp's staging tiles (free once its previous stores read them)
+            const uint32_t q16_code = smem_u32(smem + STAGES * STAGE_BYTES + 1024) + uint32_t((warp - 2) * 2 * kUgCodeTile);
+            const uint32_t q16_scale = smem_u32(smem + STAGES * STAGE_BYTES + 1024) +
+                                       uint32_t(epi_warps<kOut>() * 2 * kUgCodeTile + (warp - 2) * 1024);
+            if (kOut == kOutQ16 && P.ug_tma) {
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+            }
 #pragma unroll 1
             for (int c = half * (BN / 32) * 4 / epi_warps<kOut>(); c < (half + 1) * (BN / 32) * 4 / epi_warps<kOut>();
                  ++c) {
@@ -754,8 +763,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                             for (int k = 0; k < 4; ++k)
                                 o[k] = make_float4(y.v[4 * k], y.v[4 * k + 1], y.v[4 * k + 2], y.v[4 * k + 3]);
                         }
-                        bad |= quant16_store(y, P.q.c0 + rq * P.q.ldc + col, P.q.s0 + rq * (P.q.ldc >> 4) + (col >> 4),
-                                             -0.0f, live) & (live ? 1u : 0u);
+                        uint4 cw;
+                        uint16_t sbits;
+                        bad |= quant16(y, cw, sbits, -0.0f) & (live ? 1u : 0u);
+                        if (P.ug_tma) {
+                            // staging: code chunk (col % 128) / 16 of tile col / 128, swizzled; scale col / 16
+                            const int tcol = c * 32 + h * 16;   // column within the tile
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                             q16_code + uint32_t((tcol >> 7) * kUgCodeTile + lane * 128 +
+                                                                 ((((tcol & 127) >> 4) ^ (lane & 7)) << 4))),
+                                         "r"(cw.x), "r"(cw.y), "r"(cw.z), "r"(cw.w)
+                                         : "memory");
+                            asm volatile("st.shared.u16 [%0], %1;" ::"r"(q16_scale + uint32_t(lane * 32 + (tcol >> 4) * 2)),
+                                         "h"(sbits)
+                                         : "memory");
+                        } else if (live) {
+                            *reinterpret_cast<uint4*>(P.q.c0 + rq * P.q.ldc + col) = cw;
+                            P.q.s0[rq * (P.q.ldc >> 4) + (col >> 4)] = sbits;
+                        }
                     }
                 } else if (tma_store<kOut>() && P.tma_out) {
                     // rows / columns outside the output are clipped by the TMA unit
@@ -845,6 +870,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                     }
                 }
             }
+            if (kOut == kOutQ16 && P.ug_tma) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    // rows >= M and columns >= N are clipped by the TMA unit
+#pragma unroll
+                    for (int t = 0; t < 2; ++t)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                &emaps.c[0]),
+                            "r"(nb * BN + t * 128), "r"(row_base), "r"(q16_code + uint32_t(t * kUgCodeTile))
+                            : "memory");
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                     &emaps.s[0]),
+                                 "r"(nb * (BN / 16)), "r"(row_base), "r"(q16_scale)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -863,7 +908,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         if (kOut >= kOutQ16 && P.q.flags && __reduce_or_sync(0xFFFFFFFFu, bad) && lane == 0)
             atomicOr(P.q.flags, kFlagNonFiniteInput);
         if (tma_store<kOut>() && P.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        if (kOut == kOutUpGate && P.ug_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if ((kOut == kOutUpGate || kOut == kOutQ16) && P.ug_tma && lane == 0)
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     if (kCta >= 2) cluster_sync_all();   // no CTA of the cluster leaves while another may still signal it
@@ -983,6 +1029,12 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
                  make_map(&em.s[a], ss[a], 2, M, N / 16, 8, 32, q.ldc / 16, false);
         ug_tma = ok ? 1 : 0;
     }
+    // kOutQ16: the same for its one code array (128 x 32 boxes) and scales (16 x 32 boxes)
+    if (kOut == kOutQ16 && (q.ldc % 128) == 0)
+        ug_tma = (make_map(&em.c[0], q.c0, 1, M, N, 128, 32, q.ldc) &&
+                  make_map(&em.s[0], q.s0, 2, M, N / 16, 16, 32, q.ldc / 16, false))
+                     ? 1
+                     : 0;
     // A logical [M x K]: K-major memory [M][K]; MN-major memory [K][M]
     const bool ok_a = !kAMN ? make_map(&ma, a, ESZ, M, K, BK, BM) : make_map(&ma, a, ESZ, K, M, 128 / ESZ, BK);
     // kCta 4: the B box is a quarter (half of this CTA's half; see the producer)

@@ -83,6 +83,7 @@ def main(which):
         qg2 = coat.quantize(torch.randn(K, N2, device="cuda") / K ** 0.5, coat.QuantGeometry.per_tensor())
         qu2 = coat.quantize(torch.randn(K, N2, device="cuda") / K ** 0.5, coat.QuantGeometry.per_tensor())
         recs2 = coat.fp8_upgate_silu(qx2, qg2, qu2)
+        q16b = coat.fp8_linear_q16(qx2, qg2)   # the staged 1x16 epilogue as well
         torch.cuda.synchronize()
         assert q16.codes.shape == (M, N) and len(recs) == 4 and len(recs2) == 4
     elif which == "p2p":
