@@ -78,7 +78,7 @@ __host__ __device__ constexpr int threads_for() { return 64 + 32 * epi_warps<kOu
 #endif
 template <int kOut>
 __host__ __device__ constexpr bool tma_store() {
-    return kOut == 0 && COAT_GEMM_TMA_STORE;
+    return (kOut == 0 || kOut == 1) && COAT_GEMM_TMA_STORE;   // fp32 (128B swizzle) / bf16 (64B swizzle)
 }
 // Gate/up epilogue staging (see the kernel): per TMEM lane quarter and output
 // array (silu.in, mul.in.silu, mul.in.up) a 32-row x 128-byte code tile
@@ -789,13 +789,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                         // the store issued from this buffer two chunks ago has read it
                         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                         __syncwarp();
+                        if (kOut == kOutF32) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i)   // 16-byte chunk i of this lane's row, 128B-swizzled
-                            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                             buf + uint32_t(lane * 128 + ((i ^ (lane & 7)) << 4))),
-                                         "f"(__fmul_rn(alpha, u2f(r[4 * i]))), "f"(__fmul_rn(alpha, u2f(r[4 * i + 1]))),
-                                         "f"(__fmul_rn(alpha, u2f(r[4 * i + 2]))), "f"(__fmul_rn(alpha, u2f(r[4 * i + 3])))
-                                         : "memory");
+                            for (int i = 0; i < 8; ++i)   // 16-byte chunk i of this lane's row, 128B-swizzled
+                                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                                 buf + uint32_t(lane * 128 + ((i ^ (lane & 7)) << 4))),
+                                             "f"(__fmul_rn(alpha, u2f(r[4 * i]))),
+                                             "f"(__fmul_rn(alpha, u2f(r[4 * i + 1]))),
+                                             "f"(__fmul_rn(alpha, u2f(r[4 * i + 2]))),
+                                             "f"(__fmul_rn(alpha, u2f(r[4 * i + 3])))
+                                             : "memory");
+                        } else {
+                            // bf16: a 32 x 32 box of 64-byte rows, 64B-swizzled (chunk i ^ ((row >> 1) & 3))
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                uint32_t w[4];
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    w[j] = (f2u(round_bf16(__fmul_rn(alpha, u2f(r[8 * i + 2 * j])))) >> 16) |
+                                           (f2u(round_bf16(__fmul_rn(alpha, u2f(r[8 * i + 2 * j + 1])))) & 0xFFFF0000u);
+                                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                                 buf + uint32_t(lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4))),
+                                             "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                                             : "memory");
+                            }
+                        }
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         __syncwarp();
                         if (lane == 0) {
@@ -940,7 +958,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 2-D tensor map over a row-major matrix [rows][cols] of `esz`-byte elements,
 // box = (box_cols, box_rows), 128B swizzle, zero fill out of bounds.
 bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t cols, int box_cols, int box_rows,
-              int64_t ld = 0, bool swizzle = true) {
+              int64_t ld = 0, int swizzle = 128) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
@@ -952,7 +970,9 @@ bool make_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t c
                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUresult r = fn(m, dt, 2,
                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                          : CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -1026,13 +1046,13 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
         bool ok = true;
         for (int a = 0; a < 3 && ok; ++a)
             ok = make_map(&em.c[a], cs[a], 1, M, N, 128, 32, q.ldc) &&
-                 make_map(&em.s[a], ss[a], 2, M, N / 16, 8, 32, q.ldc / 16, false);
+                 make_map(&em.s[a], ss[a], 2, M, N / 16, 8, 32, q.ldc / 16, 0);
         ug_tma = ok ? 1 : 0;
     }
     // kOutQ16: the same for its one code array (128 x 32 boxes) and scales (16 x 32 boxes)
     if (kOut == kOutQ16 && (q.ldc % 128) == 0)
         ug_tma = (make_map(&em.c[0], q.c0, 1, M, N, 128, 32, q.ldc) &&
-                  make_map(&em.s[0], q.s0, 2, M, N / 16, 16, 32, q.ldc / 16, false))
+                  make_map(&em.s[0], q.s0, 2, M, N / 16, 16, 32, q.ldc / 16, 0))
                      ? 1
                      : 0;
     // A logical [M x K]: K-major memory [M][K]; MN-major memory [K][M]
@@ -1044,10 +1064,12 @@ cudaError_t run_cta(const void* a, const void* b, const void* b2, int M, int N, 
     const bool ok_b2 = kOut == kOutUpGate ? make_map(&mb2, b2, ESZ, K, N, 128 / ESZ, BK) : true;
     if (!ok_a || !ok_b || !ok_b2) return cudaErrorInvalidValue;
     if (kOut != kOutUpGate) mb2 = mb;
-    // tma_store(): the output [M, N] fp32 with row pitch ldo as 32 x 32 boxes (needs a 16-byte pitch)
+    // tma_store(): the output [M, N] (fp32 or bf16) with row pitch ldo as 32 x 32 boxes
+    // (128- / 64-byte rows; needs a 16-byte pitch)
     int tma_out = 0;
-    if (tma_store<kOut>() && (ldo * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0 &&
-        make_map(&mb2, out, 4, M, N, 32, 32, ldo))
+    constexpr int OSZ = kOut == kOutF32 ? 4 : 2;
+    if (tma_store<kOut>() && (ldo * OSZ) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0 &&
+        make_map(&mb2, out, OSZ, M, N, 32, 32, ldo, OSZ == 4 ? 128 : 64))
         tma_out = 1;
     auto kern = gemm_kernel<kF8, kAMN, kBMN, kOut, kCta>;
     static int attr_dev = -1;
