@@ -1141,8 +1141,9 @@ def linear_cpu_baseline(rows=16):
 def run_linear(args, extra_mode=False):
     """BASELINE.json cfg4: per-tensor FP8 E4M3 linear forward + backward with
     Group Scaling amax, Llama-2-13B MLP shape (8192 tokens x 5120 x 13824).
-    One step = Group-Scaling quantize of x (bf16) and W (fp32), fwd GEMM
-    (E4M3 x E4M3, kind::f8f6f4), dgrad (BF16, kind::f16), wgrad (BF16)."""
+    One step = Group-Scaling quantize of x (bf16) and W (fp32) -- the two
+    independent chains on two streams -- fwd GEMM (E4M3 x E4M3, kind::f8f6f4),
+    dgrad (BF16, kind::f16), wgrad (BF16)."""
     import torch
     from paper_2410_19313_b200 import _lib
     L = _lib.lib
@@ -1169,16 +1170,27 @@ def run_linear(args, extra_mode=False):
     names = ["quant", "fwd", "dgrad", "wgrad"]
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in names}
 
+    # the x and W quantization chains are independent: x's runs on a side stream
+    st2 = torch.cuda.Stream(device=dev)
+    amax_x = torch.empty(1, dtype=torch.int32, device=dev)
+    fork, join = torch.cuda.Event(), torch.cuda.Event()
+
+    def quant_chain(src, dt, rows, cols, codes, scale, am, dec, s):
+        assert L.coat_group_scale_max(src.data_ptr(), dt, rows, cols, 128, None, am.data_ptr(), s) == 0
+        assert L.coat_quantize_per_tensor(src.data_ptr(), dt, rows * cols, am.data_ptr(), codes.data_ptr(),
+                                          scale.data_ptr(), flags.data_ptr(), s) == 0
+        assert L.coat_decode_e4m3_bf16(codes.data_ptr(), dec.data_ptr(), rows * cols, s) == 0
+
     def step(rec=False):
         s = st.cuda_stream
         r = lambda k, i: ev[k][i].record(st) if rec else None
         r("quant", 0)
-        for src, dt, rows, cols, codes, scale in ((x, 1, M, K, xc, sx), (w, 0, K, N, wc, sw)):
-            assert L.coat_group_scale_max(src.data_ptr(), dt, rows, cols, 128, None, amax.data_ptr(), s) == 0
-            assert L.coat_quantize_per_tensor(src.data_ptr(), dt, rows * cols, amax.data_ptr(), codes.data_ptr(),
-                                              scale.data_ptr(), flags.data_ptr(), s) == 0
-        assert L.coat_decode_e4m3_bf16(xc.data_ptr(), xd.data_ptr(), M * K, s) == 0
-        assert L.coat_decode_e4m3_bf16(wc.data_ptr(), wd.data_ptr(), K * N, s) == 0
+        fork.record(st)
+        st2.wait_event(fork)
+        quant_chain(x, 1, M, K, xc, sx, amax_x, xd, st2.cuda_stream)
+        quant_chain(w, 0, K, N, wc, sw, amax, wd, s)
+        join.record(st2)
+        st.wait_event(join)
         r("quant", 1)
         r("fwd", 0)
         assert L.coat_fp8_linear_fwd(xc.data_ptr(), sx.data_ptr(), wc.data_ptr(), sw.data_ptr(), M, K, N,
