@@ -813,15 +813,17 @@ def run_mgaq(args, extra_mode=False):
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     nel = sum(r * c for _, r, c, *_ in bufs)
 
-    plan = os.environ.get("COAT_BENCH_MGAQ_PLAN", "rr")
+    plan = os.environ.get("COAT_BENCH_MGAQ_PLAN", "pt1")
 
     def branch_of(i):
-        """Records round-robin over the branches (as coat_quantize_batch's
-        streams).  Measured round 2: the per-tensor records all on one branch
-        (one L2-resident tensor at a time) cut the DRAM traffic from 1.17x to
-        1.12x the algorithmic bytes but serialise 8 short kernels: 0.330 vs
-        0.318 ms.  COAT_BENCH_MGAQ_PLAN=ptK (measurement): per-tensor records
-        round-robin over the first K branches, per-group over the others."""
+        """Default (COAT_BENCH_MGAQ_PLAN=pt1): the per-tensor records on branch
+        0, which runs at high stream priority, the per-group records
+        round-robin over the others -- one per-tensor record's amax and encode
+        passes at a time, so its tensor stays in L2 between them: 0.3068 vs
+        0.3090 ms for plain round robin ("rr"), DRAM traffic 1.15x vs 1.17x
+        the algorithmic bytes (without the priority the one branch is the
+        critical path: 0.323 ms).  ptK: per-tensor records over the first K
+        branches."""
         if plan.startswith("pt") and nbr > int(plan[2:]):
             k = int(plan[2:])
             G = bufs[i][3]
@@ -872,7 +874,11 @@ def run_mgaq(args, extra_mode=False):
     torch.cuda.synchronize()
     if args.mgaq_impl == "graph":
         # the layer's 9 quantizations replayed as one CUDA graph (no CPU launch gaps)
-        side = torch.cuda.Stream()
+        # branch 0 -- the per-tensor records under the default plan -- at high stream
+        # priority (the graph's kernel nodes keep it): one L2-resident per-tensor
+        # record at a time runs at full speed while the per-group records fill in
+        # (COAT_BENCH_MGAQ_PRIO=0 for the plain priority)
+        side = torch.cuda.Stream(priority=0 if os.environ.get("COAT_BENCH_MGAQ_PRIO") == "0" else -1)
         side.wait_stream(torch.cuda.current_stream())
         graph = torch.cuda.CUDAGraph()
         nb = max(1, args.mgaq_branches)
