@@ -1012,7 +1012,10 @@ def run_mgaq_fused(args, extra_mode=False):
     B = {k: (c.data_ptr(), s_.data_ptr()) for k, (c, s_) in bufs.items()}
     a0, a1, a2, a3 = (amax.data_ptr() + 4 * i for i in range(4))
 
-    branches = [torch.cuda.Stream() for _ in range(4)]
+    # COAT_BENCH_FUSED_PRIO=b (measurement): branch b (0/1 RMSNorm blocks, 2 SiLU*mul,
+    # 3 attn.out) at high stream priority
+    _fp = os.environ.get("COAT_BENCH_FUSED_PRIO", "")
+    branches = [torch.cuda.Stream(priority=-1 if _fp == str(i) else 0) for i in range(4)]
 
     def step():
         # the four blocks are independent: run them as parallel graph branches,
