@@ -32,7 +32,7 @@ def _ratio(y, ref, bound):
     return float((err / bound.clamp_min(1e-300)).max())
 
 
-@pytest.mark.parametrize("M,K,N", [(128, 256, 256), (200, 272, 400), (512, 1024, 768), (600, 512, 768),
+@pytest.mark.parametrize("M,K,N", [(16, 32, 16), (128, 256, 256), (200, 272, 400), (512, 1024, 768), (600, 512, 768),
                                    (384, 5120, 13824), (8192, 5120, 13824)])   # the last: cfg4 at full size
 def test_fp8_linear_forward(coat, M, K, N):
     import torch
@@ -65,7 +65,7 @@ def test_fp8_linear_matches_reference_loop(coat, port):
     assert np.mean(y == ref) > 0.05   # many outputs bit-identical to the sequential loop
 
 
-@pytest.mark.parametrize("M,K,N", [(256, 512, 768), (600, 256, 512), (8192, 5120, 13824)])
+@pytest.mark.parametrize("M,K,N", [(16, 32, 16), (256, 512, 768), (600, 256, 512), (8192, 5120, 13824)])
 def test_linear_dgrad(coat, M, K, N):
     import torch
     qx, qw = _quant_pair(coat, M, K, N, seed=11)
@@ -81,7 +81,7 @@ def test_linear_dgrad(coat, M, K, N):
     assert bool(ok.all()), float((err - ref.abs() * 2.0 ** -8).max())
 
 
-@pytest.mark.parametrize("M,K,N", [(384, 256, 512), (608, 1280, 512), (8192, 5120, 13824)])
+@pytest.mark.parametrize("M,K,N", [(16, 32, 16), (384, 256, 512), (608, 1280, 512), (8192, 5120, 13824)])
 def test_linear_wgrad(coat, M, K, N):
     import torch
     qx, qw = _quant_pair(coat, M, K, N, seed=17)
@@ -120,7 +120,8 @@ def _np(t):
     return t.detach().cpu().numpy()
 
 
-@pytest.mark.parametrize("M,K,N", [(128, 256, 256), (200, 272, 400), (512, 1024, 768), (8192, 4096, 11008)])
+@pytest.mark.parametrize("M,K,N", [(16, 32, 128), (128, 256, 256), (200, 272, 400), (512, 1024, 768),
+                                   (8192, 4096, 11008)])
 def test_fp8_linear_q16_epilogue(coat, port, M, K, N):
     import torch
     qx, qw = _quant_pair(coat, M, K, N, seed=M + 3 * N)
@@ -140,7 +141,7 @@ def test_fp8_linear_q16_epilogue(coat, port, M, K, N):
 
 
 # I % 128 == 0 takes the staged TMA-store epilogue (300 x 384: ragged rows), the others direct stores
-@pytest.mark.parametrize("M,H,I", [(128, 256, 256), (200, 272, 400), (300, 256, 384), (384, 512, 1040),
+@pytest.mark.parametrize("M,H,I", [(16, 32, 128), (128, 256, 256), (200, 272, 400), (300, 256, 384), (384, 512, 1040),
                                    (8192, 4096, 11008)])
 def test_fp8_upgate_silu_epilogue(coat, port, M, H, I):
     """The fused gate/up GEMM + SiLU*mul quantizers == the two forward GEMMs
