@@ -379,6 +379,35 @@ int grid_for(int64_t tiles, int per_cta) {
 // ----------------------------------------------------------------------------
 // host launchers (called by the C-ABI in api.cu)
 // ----------------------------------------------------------------------------
+cudaError_t launch_adamw_dre_step_peers(const float* w_in, float* w_out, const float* g, int64_t n,
+                                        const MomentStateIn& m_in, const MomentStateIn& v_in,
+                                        const MomentStateOut& m_out, const MomentStateOut& v_out,
+                                        const AdamWScalars& a, uint32_t* flags, const int64_t* peer_delta,
+                                        int npeers, int64_t* fused, cudaStream_t stream) {
+    *fused = 0;
+    if (n <= 0) return cudaSuccess;
+    const int64_t unit = k1_ws_round_params();
+    const int64_t nfull = n / unit;
+    int64_t done = 0;
+    if (nfull > 0) {
+        const cudaError_t e =
+            launch_k1_ws(w_in, w_out, g, nfull, m_in, v_in, m_out, v_out, a, flags, stream, peer_delta, npeers);
+        if (e == cudaSuccess) done = nfull * unit;
+        else if (e != cudaErrorNotSupported) return e;
+    }
+    *fused = done;
+    if (done == n) return cudaSuccess;
+    const int64_t gdone = done / dre::kG;
+    return launch_adamw_dre_step(w_in + done, w_out + done, g + done, n - done,
+                                 MomentStateIn{m_in.codes + done, m_in.scales + gdone, m_in.k + gdone, m_in.c + gdone},
+                                 MomentStateIn{v_in.codes + done, v_in.scales + gdone, v_in.k + gdone, v_in.c + gdone},
+                                 MomentStateOut{m_out.codes + done, m_out.scales + gdone, m_out.k + gdone,
+                                                m_out.c + gdone},
+                                 MomentStateOut{v_out.codes + done, v_out.scales + gdone, v_out.k + gdone,
+                                                v_out.c + gdone},
+                                 a, flags, nullptr, stream);
+}
+
 cudaError_t launch_adamw_dre_step(const float* w_in, float* w_out, const float* g, int64_t n,
                                   const MomentStateIn& m_in, const MomentStateIn& v_in,
                                   const MomentStateOut& m_out, const MomentStateOut& v_out,

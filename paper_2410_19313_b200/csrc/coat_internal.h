@@ -39,7 +39,17 @@ int64_t k1_ws_round_params();   // parameters per k1_ws round (2048; COAT_K1_EW=
 cudaError_t launch_k1_ws(const float* w_in, float* w_out, const float* g, int64_t nrounds,
                          const MomentStateIn& m_in, const MomentStateIn& v_in, const MomentStateOut& m_out,
                          const MomentStateOut& v_out, const AdamWScalars& a, uint32_t* flags,
-                         cudaStream_t stream);
+                         cudaStream_t stream, const int64_t* peer_delta = nullptr, int npeers = 0);
+// The step with the ZeRO all-gather fused into K1: whole rounds also store w'
+// into each peer's next-weight buffer (w_out + peer_delta[p], float offsets);
+// *fused = how many leading parameters went to the peers (the rest -- a ragged
+// tail, or everything when the fused kernel does not apply -- is the caller's
+// to broadcast).
+cudaError_t launch_adamw_dre_step_peers(const float* w_in, float* w_out, const float* g, int64_t n,
+                                        const MomentStateIn& m_in, const MomentStateIn& v_in,
+                                        const MomentStateOut& m_out, const MomentStateOut& v_out,
+                                        const AdamWScalars& a, uint32_t* flags, const int64_t* peer_delta,
+                                        int npeers, int64_t* fused, cudaStream_t stream);
 cudaError_t launch_expand_quantize_fast(const float* x, int64_t ntiles, const MomentStateOut& out,
                                         double log_target, uint32_t* flags, cudaStream_t stream);
 cudaError_t launch_dequantize_contract_fast(const MomentStateIn& in, int64_t ntiles, float* x, uint32_t* flags,

@@ -25,6 +25,7 @@
 // is set.  bf16 gradient wire: peers hold bf16 gradients (half the NVLink
 // bytes); the sum is formed in fp32 in rank order.
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/coat.h"
@@ -187,6 +188,25 @@ cudaError_t zero_p2p_step(const ZeroP2PArgs& z, const AdamWScalars& a, uint32_t*
         wp.p[r] = z.w_next_peers ? z.w_next_peers[r] : nullptr;
     }
     const int64_t n = z.n_shard, base = int64_t(z.rank) * n;
+    // P2P: fuse the all-gather into K1 (COAT_P2P_FUSED_AG=0: the separate broadcast)
+    static const bool fuse_ag = [] {
+        const char* v = getenv("COAT_P2P_FUSED_AG");
+        return !(v && v[0] == '0');
+    }();
+    int64_t peer_delta[7] = {0, 0, 0, 0, 0, 0, 0};
+    int npeers = 0;
+    const bool peer_fused = fuse_ag && !z.w_next_mc && z.w_next_peers && z.nranks > 1 && z.nranks <= 8 &&
+                            !fallbacks;
+    bool fuse_ok = peer_fused;
+    if (fuse_ok)
+        for (int r = 0; r < z.nranks; ++r)
+            if (r != z.rank) {
+                const int64_t d = int64_t(reinterpret_cast<intptr_t>(z.w_next_peers[r]) -
+                                          reinterpret_cast<intptr_t>(z.w_next));
+                if (d % int64_t(sizeof(float)) != 0) fuse_ok = false;
+                peer_delta[npeers++] = d / int64_t(sizeof(float));
+            }
+    if (!fuse_ok) npeers = 0;
     const int64_t unit = k1_ws_round_params();
     int64_t chunk = z.chunk > 0 ? z.chunk : int64_t(64) << 20;
     chunk = (chunk + unit - 1) / unit * unit;
@@ -216,20 +236,30 @@ cudaError_t zero_p2p_step(const ZeroP2PArgs& z, const AdamWScalars& a, uint32_t*
         cudaEventCreateWithFlags(&reduced, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&stepped, cudaEventDisableTiming);
         cudaEventRecord(reduced, ss.rs);
-        // the fused step on the caller's stream
+        // the fused step on the caller's stream; over P2P (no multicast) the
+        // all-gather is fused into it: K1 stores every w' into the peers'
+        // next-weight buffers as well (whole rounds; the ragged tail below)
         cudaStreamWaitEvent(stream, reduced, 0);
-        e = launch_adamw_dre_step(z.w_cur + base + off, z.w_next + base + off, z.g_shard + off, len,
-                                  slice_in(z.m_in, off), slice_in(z.v_in, off), slice_out(z.m_out, off),
-                                  slice_out(z.v_out, off), a, flags, fallbacks, stream);
+        int64_t fused = 0;
+        if (fuse_ok) {
+            e = launch_adamw_dre_step_peers(z.w_cur + base + off, z.w_next + base + off, z.g_shard + off, len,
+                                            slice_in(z.m_in, off), slice_in(z.v_in, off), slice_out(z.m_out, off),
+                                            slice_out(z.v_out, off), a, flags, peer_delta, npeers, &fused, stream);
+        } else {
+            e = launch_adamw_dre_step(z.w_cur + base + off, z.w_next + base + off, z.g_shard + off, len,
+                                      slice_in(z.m_in, off), slice_in(z.v_in, off), slice_out(z.m_out, off),
+                                      slice_out(z.v_out, off), a, flags, fallbacks, stream);
+        }
         cudaEventRecord(stepped, stream);
-        // all-gather of this chunk (ag stream, behind the step)
+        // all-gather of this chunk (ag stream, behind the step) -- what K1 did not store
         cudaStreamWaitEvent(ss.ag, stepped, 0);
-        if (z.w_next_mc)
-            broadcast_nvls_kernel<<<copy_grid(len / 4), kCopyThreads, 0, ss.ag>>>(z.w_next_mc, base + off, len / 4,
-                                                                                 z.w_next + base + off);
-        else if (z.nranks > 1)
-            broadcast_p2p_kernel<<<copy_grid(len / 4), kCopyThreads, 0, ss.ag>>>(wp, z.nranks, z.rank, base + off,
-                                                                                len / 4, z.w_next + base + off);
+        const int64_t boff = off + fused, blen = len - fused;
+        if (blen > 0 && z.w_next_mc)
+            broadcast_nvls_kernel<<<copy_grid(blen / 4), kCopyThreads, 0, ss.ag>>>(z.w_next_mc, base + boff,
+                                                                                  blen / 4, z.w_next + base + boff);
+        else if (blen > 0 && z.nranks > 1)
+            broadcast_p2p_kernel<<<copy_grid(blen / 4), kCopyThreads, 0, ss.ag>>>(
+                wp, z.nranks, z.rank, base + boff, blen / 4, z.w_next + base + boff);
         cudaEventDestroy(reduced);   // released once recorded work completes
         cudaEventDestroy(stepped);
     }
