@@ -249,7 +249,9 @@ coat_status coat_zero_step(float* w_full, const float* g_full, int64_t n_total, 
  *     given, by NVLink SHARP multimem.ld_reduce;
  *   w_next[shard] = the fused step of w_cur[shard] (coat_adamw_dre_step);
  *   every rank's next-weight buffer receives the shard: P2P stores into
- *     w_next_peers[r] (r != rank), or multimem.st into w_next_mc.
+ *     w_next_peers[r] (r != rank) -- issued by the step kernel itself right
+ *     after each local store (up to 8 ranks; a ragged chunk tail and larger
+ *     worlds by a broadcast kernel) -- or multimem.st into w_next_mc.
  * n = n_total / nranks as for coat_zero_step; w_cur / w_next are this rank's
  * full buffers (double-buffered: nothing the step reads is overwritten).
  * Stream-ordered; the caller synchronizes the ranks (e.g. an all-reduce of the
