@@ -258,3 +258,23 @@ def test_signed_zero_inputs_encode_like_reference(coat, port, geo_g, dtype):
     assert np.array_equal(q.scales.float().cpu().numpy(), scales)
     qb = coat.quantize_batch([(xt, geo)])[0]
     assert np.array_equal(qb.codes.cpu().numpy(), codes)
+
+
+@pytest.mark.parametrize("n", [256, 4099, 1 << 20])
+def test_decode_e4m3_bf16_exact(coat, n):
+    """coat_decode_e4m3_bf16 (the BF16 code values for the backward GEMMs): the
+    vectorized 16-codes-per-thread kernel and the scalar tail give exactly the
+    top half of the fp32 decode (<= 4 significant bits: exact in BF16); NaN
+    codes decode to a NaN."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(n)
+    codes = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda", generator=g)
+    codes[:256] = torch.arange(256, dtype=torch.uint8, device="cuda")
+    out = coat.decode_e4m3_bf16(codes)
+    ref = coat.decode_e4m3(codes)
+    torch.cuda.synchronize()
+    nan = torch.isnan(ref)
+    assert bool(torch.isnan(out.float())[nan].all())
+    got = out.view(torch.int16)[~nan]
+    want = (ref.view(torch.int32)[~nan] >> 16).to(torch.int16)
+    assert torch.equal(got, want)
