@@ -656,7 +656,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 if (P.ug_tma) {
                     // the previous tile's stores have read the staging tiles
                     if (ug_issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+                    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "n"(8 * epi_warps<kOut>()) : "memory");
                 }
 #pragma unroll 1
                 for (int gi = half * kGroups; gi < (half + 1) * kGroups; ++gi) {
@@ -705,7 +705,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
                 }
                 if (P.ug_tma) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+                    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "n"(8 * epi_warps<kOut>()) : "memory");
                     if (ug_issuer) {
                         // rows >= M and columns >= N are clipped by the TMA unit
 #pragma unroll
