@@ -65,7 +65,8 @@ def test_fp8_linear_matches_reference_loop(coat, port):
     assert np.mean(y == ref) > 0.05   # many outputs bit-identical to the sequential loop
 
 
-@pytest.mark.parametrize("M,K,N", [(16, 32, 16), (256, 512, 768), (600, 256, 512), (8192, 5120, 13824)])
+@pytest.mark.parametrize("M,K,N", [(16, 32, 16), (256, 512, 768), (600, 256, 512), (200, 272, 400),
+                                   (8192, 5120, 13824)])   # 272: a partial 32-column bf16 output chunk
 def test_linear_dgrad(coat, M, K, N):
     import torch
     qx, qw = _quant_pair(coat, M, K, N, seed=11)
@@ -81,7 +82,8 @@ def test_linear_dgrad(coat, M, K, N):
     assert bool(ok.all()), float((err - ref.abs() * 2.0 ** -8).max())
 
 
-@pytest.mark.parametrize("M,K,N", [(16, 32, 16), (384, 256, 512), (608, 1280, 512), (8192, 5120, 13824)])
+@pytest.mark.parametrize("M,K,N", [(16, 32, 16), (384, 256, 512), (608, 1280, 512), (208, 272, 400),
+                                   (8192, 5120, 13824)])
 def test_linear_wgrad(coat, M, K, N):
     import torch
     qx, qw = _quant_pair(coat, M, K, N, seed=17)
