@@ -40,14 +40,14 @@ def assert_state_equal(got, exp, what=""):
         assert bad.size == 0, (what, key, bad[:8], a[bad[:8]], b[bad[:8]])
 
 
-def run_both(coat, port, n, steps, cfg=CFG, seed=1, warm=None, grad_scale=1e-3):
+def run_both(coat, port, n, steps, cfg=CFG, seed=1, warm=None, grad_scale=1e-3, t_start=9):
     w0 = port.generate(0, (n,), 0.0, 100.0, seed) * np.float32(0.02)
     w_ref = w0.copy()
     m, v = port.make_slot(n)
     slot = coat.make_slot([n])
     if warm is not None:
         m, v = warm
-        slot.load_state(m, v, 9)
+        slot.load_state(m, v, t_start)
         m = {k: a.copy() for k, a in m.items()}
         v = {k: a.copy() for k, a in v.items()}
     t0 = slot.step
@@ -71,8 +71,11 @@ def test_step_trajectory_bit_exact(coat, port, checker, n):
     run_both(coat, checker, n, 5)
 
 
-def test_step_from_warmed_state(coat, port, checker):
-    """Fixture (B) of SURVEY.md 8(d): m with k ~ 1-3, v with k ~ 5-15, t = 10."""
+@pytest.mark.parametrize("t_start", [9, 160, 20000])
+def test_step_from_warmed_state(coat, port, checker, t_start):
+    """Fixture (B) of SURVEY.md 8(d): m with k ~ 1-3, v with k ~ 5-15, t = 10;
+    also late in a run: t = 161 (bc1 one ulp below 1) and t = 20001 (bc1 =
+    bc2 = 1 exactly in fp32: the Markstein divisions by 1)."""
     groups = 2048
     n = groups * 128
     m0 = port.generate(0, (n,), 0.01, 100.0, 21) * np.float32(1e-4)
@@ -82,7 +85,7 @@ def test_step_from_warmed_state(coat, port, checker):
     mc, ms, mk, mcc = checker.expand_quantize(m0)
     vc, vs, vk, vcc = checker.expand_quantize(v0)
     warm = ({"codes": mc, "scales": ms, "k": mk, "c": mcc}, {"codes": vc, "scales": vs, "k": vk, "c": vcc})
-    run_both(coat, checker, n, 3, warm=warm)
+    run_both(coat, checker, n, 3, warm=warm, t_start=t_start)
 
 
 def test_step_sparse_zero_and_extreme_groups(coat, port, checker):
