@@ -1206,15 +1206,17 @@ def run_linear(args, extra_mode=False):
         fork.record(st)
         st2.wait_event(fork)
         quant_chain(x, 1, M, K, xc, sx, amax_x, st2.cuda_stream)
+        if not overlap_dec:
+            assert L.coat_decode_e4m3_bf16(xc.data_ptr(), xd.data_ptr(), M * K, st2.cuda_stream) == 0
         quant_chain(w, 0, K, N, wc, sw, amax, s)
+        if not overlap_dec:
+            assert L.coat_decode_e4m3_bf16(wc.data_ptr(), wd.data_ptr(), K * N, s) == 0
         join.record(st2)
         st.wait_event(join)
         if overlap_dec:
             st3.wait_stream(st)
             decodes(st3.cuda_stream)
             decoded.record(st3)
-        else:
-            decodes(s)
         r("quant", 1)
         r("fwd", 0)
         assert L.coat_fp8_linear_fwd(xc.data_ptr(), sx.data_ptr(), wc.data_ptr(), sw.data_ptr(), M, K, N,
