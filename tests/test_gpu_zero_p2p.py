@@ -328,18 +328,21 @@ def test_p2p_step_separate_processes_ipc(checker, ws):
     assert np.array_equal(mine["k"], m["k"][:n // 128]) and np.array_equal(mine["c"], m["c"][:n // 128])
 
 
-def test_p2p_step_separate_broadcast_path():
+@pytest.mark.parametrize("env", [{"COAT_P2P_FUSED_AG": "0"}, {"COAT_K1_EW": "7"}],
+                         ids=["separate-broadcast", "ew7-fallback"])
+def test_p2p_step_separate_broadcast_path(env):
     """COAT_P2P_FUSED_AG=0: the all-gather by the separate P2P broadcast kernel
-    instead of K1's own peer stores -- the virtual-rank parity cases pass on it
-    too (the default runs them with the all-gather fused into K1)."""
+    instead of K1's own peer stores; COAT_K1_EW=7: the fused variant exists
+    for the default layout only, so the step falls back to the broadcast --
+    the virtual-rank parity cases pass on both (the default runs them with the
+    all-gather fused into K1)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, COAT_P2P_FUSED_AG="0")
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                           "tests/test_gpu_zero_p2p.py", "-k", "virtual_ranks"],
-                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+                         cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     tail = (out.stdout + out.stderr)[-3000:]
     assert out.returncode == 0, tail
     assert " passed" in out.stdout and " failed" not in out.stdout, tail
